@@ -1,0 +1,165 @@
+/*
+ * fkt_cuda.h — C-ABI of the B200-native Fast Kernel Transform MVM.
+ *
+ * Plain C: opaque handles, pointers and sizes, int status codes and a
+ * thread-local message (no C++ exceptions cross this boundary). The C++
+ * operator API in include/fkt/*.hpp (a drop-in for the reference's
+ * proj/include/fkt) and the Python mirror (paper_2106_04487_b200) are thin
+ * layers over these entry points; see INTEGRATION.md.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef FKT_CUDA_H
+#define FKT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; each maps to a reference exception type. */
+enum {
+  FKT_OK = 0,
+  FKT_ERR_INVALID_ARGUMENT = 1,   /* std::invalid_argument */
+  FKT_ERR_DIMENSION_MISMATCH = 2, /* fkt::DimensionMismatchError (transform.hpp:17-20) */
+  FKT_ERR_ORDER_TOO_LARGE = 3,    /* fkt::OrderTooLargeError (coefficients.hpp:23-28) */
+  FKT_ERR_NOT_RECURRENCE = 4,     /* fkt::NotRecurrenceKernelError (expansion.hpp:27-31) */
+  FKT_ERR_SINGULAR_AT_ZERO = 5,   /* fkt::SingularAtZeroError (kernels.hpp:22-26) */
+  FKT_ERR_ZERO_REFERENCE = 6,     /* fkt::ZeroReferenceError (transform.hpp:22-25) */
+  FKT_ERR_CUDA = 7,               /* device failure (no CPU fallback exists) */
+  FKT_ERR_UNSUPPORTED = 8,        /* valid for the reference, not offered on the GPU path */
+  FKT_ERR_INTERNAL = 9
+};
+
+/* Compression modes, reference transform.hpp:27. */
+enum { FKT_COMPRESSION_AUTO = 0, FKT_COMPRESSION_ON = 1, FKT_COMPRESSION_OFF = 2 };
+
+/* Reference fkt::FktOptions (transform.hpp:29-41). */
+typedef struct fkt_options {
+  int p;
+  double theta;
+  int leaf_capacity;
+  int compression;
+  int eager_operators; /* accepted; the GPU always recomputes operators in registers */
+  int barnes_hut;      /* not offered on the GPU path (FKT_ERR_UNSUPPORTED) */
+  int threads;         /* CPU-only knob, ignored */
+  int has_diagonal;
+  double diagonal;
+} fkt_options;
+
+typedef struct fkt_plan_s* fkt_plan_t;
+typedef struct fkt_tree_s* fkt_tree_t;
+
+typedef struct fkt_plan_info {
+  int n, d, p;
+  long long nodes, leaves, depth;
+  long long far_total, near_total;
+  long long coefficient_count; /* reference FktPlan::coefficientCount() */
+  long long stored_coefficients;
+  int compressed;              /* reference FktPlan::compressed() */
+  double plan_seconds;
+  long long far_tiles, near_tiles, s2m_tiles;
+} fkt_plan_info;
+
+/* Last error message / code of the calling thread. */
+const char* fkt_last_error(void);
+int fkt_last_error_code(void);
+
+/* Library version string and the 14 built-in kernel names
+ * (reference builtinKernelNames(), kernels.hpp:85). */
+const char* fkt_version(void);
+int fkt_kernel_count(void);
+const char* fkt_kernel_name(int i);
+
+/* Kernel validation and host evaluation (reference makeKernel, kernels.hpp:83,
+ * IsotropicKernel::operator(), kernels.hpp:49-58). Parameters are parallel
+ * key/value arrays. */
+int fkt_kernel_check(const char* name, const char* const* keys, const double* values, int nparams,
+                     int* has_recurrence, int* has_value_at_zero, double* value_at_zero);
+int fkt_kernel_eval(const char* name, const char* const* keys, const double* values, int nparams,
+                    const double* r, double* out, long long count, int has_diagonal, double diagonal);
+
+void fkt_default_options(fkt_options* opt);
+
+/* fkt::FktPlan(PointCloud, KernelPtr, FktOptions) — transform.cpp:39-92.
+ * x: host, row-major n x d. */
+int fkt_plan_create(int n, int d, const double* x, const char* kernel, const char* const* keys,
+                    const double* values, int nparams, const fkt_options* opt, fkt_plan_t* out);
+int fkt_plan_destroy(fkt_plan_t plan);
+int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info);
+
+/* fkt::FktPlan::multiply(span y) — transform.cpp:184-204. Host buffers,
+ * synchronous; nrhs column-major right-hand sides (length n*nrhs). */
+int fkt_plan_multiply(fkt_plan_t plan, const double* y, double* z, int nrhs);
+/* Same on device buffers, enqueued on `stream` (cudaStream_t; NULL = the
+ * plan's own stream, synchronised before return). */
+int fkt_plan_multiply_device(fkt_plan_t plan, const double* y_dev, double* z_dev, int nrhs, void* stream);
+/* Stage-level device calls used by the benchmark to time kernels. stage:
+ * 0 gather, 1 s2m, 2 near, 3 m2t, 4 scatter (workspaces owned by the plan). */
+int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, double* z_dev, int nrhs, void* stream);
+
+/* Tree view of a plan (borrowed; valid while the plan lives). */
+fkt_tree_t fkt_plan_tree(fkt_plan_t plan);
+
+/* fkt::PartitionTree(cloud, leafCapacity) + computeInteractionSets(theta) —
+ * tree.hpp:43-79, tree.cpp:29-213. Built on the GPU. */
+int fkt_tree_create(int n, int d, const double* x, int leaf_capacity, fkt_tree_t* out);
+int fkt_tree_compute_sets(fkt_tree_t tree, double theta);
+int fkt_tree_destroy(fkt_tree_t tree);
+/* nodes, depth, far/near totals (0 before computeInteractionSets), theta */
+int fkt_tree_sizes(fkt_tree_t tree, long long* nodes, long long* depth, long long* far_total,
+                   long long* near_total, double* theta);
+/* Node arrays in reference pre-order (tree.hpp:30-41); any pointer may be NULL.
+ * center/box_lo/box_hi: nodes x d. */
+int fkt_tree_nodes(fkt_tree_t tree, uint32_t* begin, uint32_t* end, int* left, int* right, double* radius,
+                   double* center, double* box_lo, double* box_hi);
+/* PartitionTree::order() (permuted position -> original index) and the
+ * permuted coordinates pointAt(pos) (n x d row-major). */
+int fkt_tree_order(fkt_tree_t tree, uint32_t* order);
+int fkt_tree_points(fkt_tree_t tree, double* perm);
+/* farSet / nearSet of every node as CSR of ORIGINAL indices, ascending
+ * (tree.hpp:37-38); off has nodes+1 entries. */
+int fkt_tree_far_sets(fkt_tree_t tree, long long* off, uint32_t* idx);
+int fkt_tree_near_sets(fkt_tree_t tree, long long* off, uint32_t* idx);
+
+/* fkt::denseMultiply (transform.cpp:210-237) on the GPU, and a sampled-row
+ * variant (rows: original indices). Host buffers. */
+int fkt_dense_multiply(int n, int d, const double* x, const char* kernel, const char* const* keys,
+                       const double* values, int nparams, const double* y, double* z, int has_diagonal,
+                       double diagonal);
+int fkt_dense_rows(int n, int d, const double* x, const char* kernel, const char* const* keys,
+                   const double* values, int nparams, const double* y, int m, const int64_t* rows,
+                   double* z, int has_diagonal, double diagonal);
+
+/* fkt::relativeError (transform.cpp:245-255). */
+int fkt_relative_error(const double* approx, const double* exact, long long n, double* out);
+
+/* fkt::expansionSize (expansion.hpp:34): binom(d+p, p). */
+long long fkt_expansion_size(int d, int p);
+
+/* Plan-time expansion tables (host, no GPU needed): exact T-bar_kjm
+ * (coefficients.hpp:47-52) as a double and as "num/den" text; the exact
+ * compression ranks per degree (expansion.cpp:190-243; -1 entries when the
+ * kernel has no recurrence -> FKT_ERR_NOT_RECURRENCE); Z_k
+ * (harmonics.hpp:56). */
+int fkt_tbar(int d, int p, int k, int j, int m, double* value, char* exact, int exact_len);
+int fkt_compression_ranks(const char* kernel, const char* const* keys, const double* values, int nparams, int d,
+                          int p, int* ranks);
+double fkt_addition_normalizer(int d, int k);
+long long fkt_harmonic_count(int d, int k);
+
+/* Seeded synthetic inputs (reference fkt::Rng, synthetic.hpp:17-50;
+ * generators synthetic.cpp:7-55). kind: "cube", "sphere", "mixture".
+ * y (optional) receives normalVector(n) drawn after the cloud. */
+int fkt_synth_cloud(const char* kind, int n, int d, uint64_t seed, double* x, double* y);
+/* The five BASELINE configurations (SURVEY Appendix B recipes). */
+int fkt_synth_config(int cfg, int n, uint64_t seed, double* x, double* w);
+int fkt_config_dims(int cfg, int* d, int* nrhs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FKT_CUDA_H */

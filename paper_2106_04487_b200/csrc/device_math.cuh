@@ -1,0 +1,468 @@
+// Device math for the FKT kernels (sm_100a): isotropic kernel evaluation
+// (near field, dense rows), Taylor jets of the kernels (far-field radial
+// coefficients) and raw hyperspherical-harmonic chains (s2m / m2t).
+//
+// Reference map:
+//  * kernel formulas      proj/src/kernels.cpp:37-156
+//  * jet arithmetic       proj/include/fkt/jet.hpp:88-210
+//  * harmonic chains      proj/src/harmonics.cpp:160-246 (normalisation
+//                          constants are folded into the node moments on the
+//                          host side, see far.cu)
+#ifndef FKTB_DEVICE_MATH_CUH
+#define FKTB_DEVICE_MATH_CUH
+
+#include "fkt_device_types.h"
+
+namespace fktb {
+
+// ---------------------------------------------------------------------------
+// K(r) for r > 0 given dist2 = r^2 (and r when the formula needs it). Where the
+// reference formula only involves r^2 the square root is skipped; the value
+// differs from reference bits by roundoff only.
+template <int KID>
+struct KernelNeedsR {
+  static constexpr bool value = !(KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC ||
+                                  KID == FKTB_KERNEL_GAUSSIAN || KID == FKTB_KERNEL_INVERSE_R ||
+                                  KID == FKTB_KERNEL_INVERSE_R2 || KID == FKTB_KERNEL_EXP_NEG_INV_R2);
+};
+
+template <int KID>
+__device__ __forceinline__ double kernel_value(const FktbKernelDesc& k, double dist2) {
+  if constexpr (KID == FKTB_KERNEL_CAUCHY) {
+    return 1.0 / fma(dist2, k.is2, 1.0);
+  } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
+    return rsqrt(fma(dist2, k.is2, 1.0));
+  } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
+    return exp(-dist2);
+  } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
+    return rsqrt(dist2);
+  } else if constexpr (KID == FKTB_KERNEL_INVERSE_R2) {
+    return 1.0 / dist2;
+  } else if constexpr (KID == FKTB_KERNEL_EXP_NEG_INV_R2) {
+    return exp(-(1.0 / dist2));
+  } else {
+    const double r = sqrt(dist2);
+    if constexpr (KID == FKTB_KERNEL_EXPONENTIAL) return exp(-r);
+    if constexpr (KID == FKTB_KERNEL_MATERN12) return k.s2 * exp(-r / k.rho);
+    if constexpr (KID == FKTB_KERNEL_MATERN32) {
+      const double ar = k.a * r;
+      return k.s2 * (1.0 + ar) * exp(-ar);
+    }
+    if constexpr (KID == FKTB_KERNEL_INVERSE_R3) return 1.0 / (r * dist2);
+    if constexpr (KID == FKTB_KERNEL_EXP_OVER_R) return exp(-r) / r;
+    if constexpr (KID == FKTB_KERNEL_R_EXP) return r * exp(-r);
+    if constexpr (KID == FKTB_KERNEL_COS_OVER_R) return cos(r) / r;
+    if constexpr (KID == FKTB_KERNEL_EXP_NEG_INV_R) return exp(-(1.0 / r));
+    return 0.0;
+  }
+}
+
+// Runtime-dispatched K(r), r > 0 (far-field compressed path).
+__device__ __forceinline__ double kernel_value_rt(const FktbKernelDesc& k, double r) {
+  const double r2 = r * r;
+  switch (k.id) {
+    case FKTB_KERNEL_EXPONENTIAL: return exp(-r);
+    case FKTB_KERNEL_MATERN12: return k.s2 * exp(-r / k.rho);
+    case FKTB_KERNEL_MATERN32: return k.s2 * (1.0 + k.a * r) * exp(-(k.a * r));
+    case FKTB_KERNEL_CAUCHY: return 1.0 / (1.0 + r2 * k.is2);
+    case FKTB_KERNEL_RATIONAL_QUADRATIC: return 1.0 / sqrt(1.0 + r2 * k.is2);
+    case FKTB_KERNEL_GAUSSIAN: return exp(-r2);
+    case FKTB_KERNEL_INVERSE_R: return 1.0 / r;
+    case FKTB_KERNEL_INVERSE_R2: return 1.0 / r2;
+    case FKTB_KERNEL_INVERSE_R3: return 1.0 / (r2 * r);
+    case FKTB_KERNEL_EXP_OVER_R: return exp(-r) / r;
+    case FKTB_KERNEL_R_EXP: return r * exp(-r);
+    case FKTB_KERNEL_COS_OVER_R: return cos(r) / r;
+    case FKTB_KERNEL_EXP_NEG_INV_R: return exp(-(1.0 / r));
+    case FKTB_KERNEL_EXP_NEG_INV_R2: return exp(-(1.0 / r2));
+  }
+  return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Truncated Taylor series of order N (coefficient m = f^(m)(r)/m!). The
+// recurrences restate proj/include/fkt/jet.hpp:110-190; with N a compile-time
+// constant everything stays in registers. `n` is the runtime order (<= N).
+template <int N>
+struct Jet {
+  double c[N + 1];
+};
+
+template <int N>
+__device__ __forceinline__ void jet_mul(const Jet<N>& a, const Jet<N>& b, Jet<N>& r, int n) {
+#pragma unroll
+  for (int i = 0; i <= N; ++i) {
+    if (i > n) break;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j <= i; ++j) acc = fma(a.c[j], b.c[i - j], acc);
+    r.c[i] = acc;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_div(const Jet<N>& a, const Jet<N>& b, Jet<N>& r, int n) {
+  const double inv = 1.0 / b.c[0];
+#pragma unroll
+  for (int i = 0; i <= N; ++i) {
+    if (i > n) break;
+    double acc = a.c[i];
+#pragma unroll
+    for (int j = 1; j <= i; ++j) acc = fma(-b.c[j], r.c[i - j], acc);
+    r.c[i] = acc * inv;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_recip(const Jet<N>& b, Jet<N>& r, int n) {
+  const double inv = 1.0 / b.c[0];
+#pragma unroll
+  for (int i = 0; i <= N; ++i) {
+    if (i > n) break;
+    double acc = i == 0 ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = 1; j <= i; ++j) acc = fma(-b.c[j], r.c[i - j], acc);
+    r.c[i] = acc * inv;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_exp(const Jet<N>& f, Jet<N>& g, int n) {
+  g.c[0] = exp(f.c[0]);
+#pragma unroll
+  for (int m = 1; m <= N; ++m) {
+    if (m > n) break;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 1; k <= m; ++k) acc = fma(static_cast<double>(k) * f.c[k], g.c[m - k], acc);
+    g.c[m] = acc * (1.0 / m);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_sqrt(const Jet<N>& f, Jet<N>& g, int n) {
+  g.c[0] = sqrt(f.c[0]);
+  const double inv2 = 0.5 / g.c[0];
+#pragma unroll
+  for (int m = 1; m <= N; ++m) {
+    if (m > n) break;
+    double acc = f.c[m];
+#pragma unroll
+    for (int k = 1; k < m; ++k) acc = fma(-g.c[k], g.c[m - k], acc);
+    g.c[m] = acc * inv2;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_cos(const Jet<N>& f, Jet<N>& cj, int n) {
+  Jet<N> s;
+  s.c[0] = sin(f.c[0]);
+  cj.c[0] = cos(f.c[0]);
+#pragma unroll
+  for (int m = 1; m <= N; ++m) {
+    if (m > n) break;
+    double sa = 0.0, ca = 0.0;
+#pragma unroll
+    for (int k = 1; k <= m; ++k) {
+      const double kf = k * f.c[k];
+      sa = fma(kf, cj.c[m - k], sa);
+      ca = fma(-kf, s.c[m - k], ca);
+    }
+    s.c[m] = sa * (1.0 / m);
+    cj.c[m] = ca * (1.0 / m);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void jet_scale(Jet<N>& a, double s, int n) {
+#pragma unroll
+  for (int i = 0; i <= N; ++i)
+    if (i <= n) a.c[i] *= s;
+}
+
+template <int N>
+__device__ __forceinline__ void jet_var(double r, Jet<N>& v, int n) {
+#pragma unroll
+  for (int i = 0; i <= N; ++i) v.c[i] = 0.0;
+  v.c[0] = r;
+  if (n >= 1) v.c[1] = 1.0;
+}
+
+// Jet of the kernel at r > 0 up to order n (reference kernels.hpp:61-64 with
+// the generic lambdas of kernels.cpp). Closed forms where they are short.
+template <int N>
+__device__ __forceinline__ void kernel_jet(const FktbKernelDesc& k, double r, Jet<N>& out, int n) {
+  switch (k.id) {
+    case FKTB_KERNEL_EXPONENTIAL:
+    case FKTB_KERNEL_MATERN12: {
+      // c_m = s (-1/l)^m e^{-r/l} / m!
+      const double il = k.id == FKTB_KERNEL_EXPONENTIAL ? 1.0 : 1.0 / k.rho;
+      const double s = k.id == FKTB_KERNEL_EXPONENTIAL ? 1.0 : k.s2;
+      double t = s * exp(-r * il);
+#pragma unroll
+      for (int m = 0; m <= N; ++m) {
+        out.c[m] = t;
+        t *= -il / (m + 1);
+      }
+      return;
+    }
+    case FKTB_KERNEL_MATERN32: {
+      // d^m/dr^m (1 + a r) e^{-a r} = (-a)^m (a r - m + 1) e^{-a r}
+      const double ar = k.a * r;
+      double t = k.s2 * exp(-ar);
+#pragma unroll
+      for (int m = 0; m <= N; ++m) {
+        out.c[m] = t * (ar - m + 1.0);
+        t *= -k.a / (m + 1);
+      }
+      return;
+    }
+    case FKTB_KERNEL_INVERSE_R: {
+      // c_m = (-1)^m r^{-m-1}
+      const double ir = 1.0 / r;
+      double t = ir;
+#pragma unroll
+      for (int m = 0; m <= N; ++m) {
+        out.c[m] = t;
+        t *= -ir;
+      }
+      return;
+    }
+    default:
+      break;
+  }
+  Jet<N> v, a, b;
+  jet_var(r, v, n);
+  switch (k.id) {
+    case FKTB_KERNEL_CAUCHY:
+    case FKTB_KERNEL_RATIONAL_QUADRATIC:
+      jet_mul(v, v, a, n);
+      jet_scale(a, k.is2, n);
+      a.c[0] += 1.0;
+      if (k.id == FKTB_KERNEL_CAUCHY) {
+        jet_recip(a, out, n);
+      } else {
+        jet_sqrt(a, b, n);
+        jet_recip(b, out, n);
+      }
+      return;
+    case FKTB_KERNEL_GAUSSIAN:
+      jet_mul(v, v, a, n);
+      jet_scale(a, -1.0, n);
+      jet_exp(a, out, n);
+      return;
+    case FKTB_KERNEL_INVERSE_R2:
+      jet_mul(v, v, a, n);
+      jet_recip(a, out, n);
+      return;
+    case FKTB_KERNEL_INVERSE_R3:
+      jet_mul(v, v, a, n);
+      jet_mul(a, v, b, n);
+      jet_recip(b, out, n);
+      return;
+    case FKTB_KERNEL_EXP_OVER_R:
+      jet_scale(v, -1.0, n);
+      jet_exp(v, a, n);
+      jet_var(r, v, n);
+      jet_div(a, v, out, n);
+      return;
+    case FKTB_KERNEL_R_EXP:
+      jet_scale(v, -1.0, n);
+      jet_exp(v, a, n);
+      jet_var(r, v, n);
+      jet_mul(v, a, out, n);
+      return;
+    case FKTB_KERNEL_COS_OVER_R:
+      jet_cos(v, a, n);
+      jet_div(a, v, out, n);
+      return;
+    case FKTB_KERNEL_EXP_NEG_INV_R:
+      jet_recip(v, a, n);
+      jet_scale(a, -1.0, n);
+      jet_exp(a, out, n);
+      return;
+    case FKTB_KERNEL_EXP_NEG_INV_R2:
+      jet_mul(v, v, a, n);
+      jet_recip(a, b, n);
+      jet_scale(b, -1.0, n);
+      jet_exp(b, out, n);
+      return;
+    default:
+#pragma unroll
+      for (int m = 0; m <= N; ++m) out.c[m] = 0.0;
+      return;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compile-time harmonic chain tables (same enumeration as
+// proj/src/harmonics.cpp:62-103): for each harmonic, the Gegenbauer table
+// entry per level, the circular index and the cos/sin phase.
+constexpr int harmonic_count_deg(int d, int k) {
+  // binom(k+d-1, k) - binom(k+d-3, k-2)
+  auto binom = [](int n, int r) -> long long {
+    if (r < 0 || n < 0 || r > n) return 0;
+    long long b = 1;
+    for (int i = 1; i <= r; ++i) b = b * (n - r + i) / i;
+    return b;
+  };
+  return static_cast<int>(binom(k + d - 1, k) - binom(k + d - 3, k - 2));
+}
+
+constexpr int harmonic_count(int d, int p) {
+  int h = 0;
+  for (int k = 0; k <= p; ++k) h += harmonic_count_deg(d, k);
+  return h;
+}
+
+constexpr int harmonic_offset(int d, int k) {
+  int h = 0;
+  for (int q = 0; q < k; ++q) h += harmonic_count_deg(d, q);
+  return h;
+}
+constexpr int slots_u(int p, int k) { return (p - k) / 2 + 1; }
+constexpr int slot_base(int p, int k) {
+  int s = 0;
+  for (int q = 0; q < k; ++q) s += slots_u(p, q);
+  return s;
+}
+constexpr int coef_offset(int d, int p, int k) {
+  int c = 0;
+  for (int q = 0; q < k; ++q) c += harmonic_count_deg(d, q) * slots_u(p, q);
+  return c;
+}
+
+// Per-level Gegenbauer table g[level][m][n], n <= P - m: flat offset.
+constexpr int g_level_size(int P) { return (P + 1) * (P + 2) / 2; }
+constexpr int g_index(int P, int level, int m, int n) {
+  return (level - 1) * g_level_size(P) + (m * (2 * P + 3 - m)) / 2 + n;
+}
+
+template <int D, int P>
+struct ChainTable {
+  static constexpr int H = harmonic_count(D, P);
+  static constexpr int L = D > 2 ? D - 2 : 1;
+  int gi[H][L];
+  int ci[H];
+  int ph[H];
+  int deg[H];
+};
+
+template <int D, int P>
+constexpr ChainTable<D, P> make_chain_table() {
+  ChainTable<D, P> t{};
+  int h = 0;
+  for (int k = 0; k <= P; ++k) {
+    if (D == 2) {
+      if (k == 0) {
+        t.gi[h][0] = -1;
+        t.ci[h] = 0;
+        t.ph[h] = 0;
+        t.deg[h] = 0;
+        ++h;
+      } else {
+        for (int s = 0; s < 2; ++s) {
+          t.gi[h][0] = -1;
+          t.ci[h] = k;
+          t.ph[h] = s == 0 ? 1 : -1;
+          t.deg[h] = k;
+          ++h;
+        }
+      }
+      continue;
+    }
+    // Iterative enumeration of m_1 >= ... >= m_{D-2}, nested ascending loops.
+    int m[D > 2 ? D - 1 : 1] = {};
+    m[0] = k;
+    int level = 1;
+    for (int i = 1; i < D - 1; ++i) m[i] = 0;
+    while (true) {
+      // emit chain with m[1..D-2]
+      const int last = m[D - 2];
+      for (int s = 0; s < (last > 0 ? 2 : 1); ++s) {
+        for (int l = 1; l <= D - 2; ++l) t.gi[h][l - 1] = g_index(P, l, m[l], m[l - 1] - m[l]);
+        t.ci[h] = last;
+        t.ph[h] = last == 0 ? 0 : (s == 0 ? 1 : -1);
+        t.deg[h] = k;
+        ++h;
+      }
+      // advance odometer from the deepest level
+      level = D - 2;
+      while (level >= 1) {
+        if (m[level] < m[level - 1]) {
+          ++m[level];
+          for (int l = level + 1; l <= D - 2; ++l) m[l] = 0;
+          break;
+        }
+        --level;
+      }
+      if (level < 1) break;
+    }
+  }
+  return t;
+}
+
+// Raw (unnormalised) harmonic values Yraw[h] at relative position x (any
+// scale, the direction is taken). For x = 0 every degree >= 1 vanishes and
+// Yraw[0] = 1, which is the collocated-source rule of
+// proj/src/expansion.cpp:273-289 once the norm is folded in.
+template <int D, int P>
+__device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, double (&Y)[ChainTable<D, P>::H]) {
+  constexpr ChainTable<D, P> T = make_chain_table<D, P>();
+  const double inv = r > 0.0 ? 1.0 / r : 0.0;
+  double v[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = x[a] * inv;
+  double cA[P + 1], cB[P + 1];
+  cA[0] = 1.0;
+  cB[0] = 0.0;
+  const double cx = v[D - 2], cy = v[D - 1];
+#pragma unroll
+  for (int m = 1; m <= P; ++m) {
+    cA[m] = cA[m - 1] * cx - cB[m - 1] * cy;
+    cB[m] = cB[m - 1] * cx + cA[m - 1] * cy;
+  }
+  if constexpr (D == 2) {
+#pragma unroll
+    for (int h = 0; h < T.H; ++h) Y[h] = T.ph[h] >= 0 ? cA[T.ci[h]] : cB[T.ci[h]];
+  } else {
+    double tail[D - 1];
+    {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) {
+        acc += v[i] * v[i];
+        if (i <= D - 2) tail[i] = acc;
+      }
+    }
+    double g[(D - 2) * g_level_size(P)];
+#pragma unroll
+    for (int level = 1; level <= D - 2; ++level) {
+      const double xx = v[level - 1];
+      const double t2 = tail[level - 1];
+#pragma unroll
+      for (int m = 0; m <= P; ++m) {
+        const int twoLam = D - 1 - level + 2 * m;  // 2 * lambda
+        double* row = g + g_index(P, level, m, 0);
+        row[0] = 1.0;
+        if (P - m >= 1) row[1] = static_cast<double>(twoLam) * xx;
+#pragma unroll
+        for (int n = 2; n <= P - m; ++n)
+          row[n] = (static_cast<double>(2 * n + twoLam - 2) * xx * row[n - 1] -
+                    static_cast<double>(n + twoLam - 2) * t2 * row[n - 2]) *
+                   (1.0 / n);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < T.H; ++h) {
+      double prod = T.ph[h] >= 0 ? cA[T.ci[h]] : cB[T.ci[h]];
+#pragma unroll
+      for (int l = 0; l < D - 2; ++l) prod *= g[T.gi[h][l]];
+      Y[h] = prod;
+    }
+  }
+}
+
+}  // namespace fktb
+
+#endif

@@ -1,0 +1,153 @@
+// K3: near field (reference proj/src/transform.cpp:163-181).
+//
+// For every leaf l and target t in its near set N_l:
+//   z_t += sum_{s in l} K(|x_t - x_s|) y_s      (K(0) -> diagonal convention)
+// Work tiles are (leaf, <= kNearTile targets of N_l). One CTA stages the
+// leaf's sources (SoA coordinates + weights, contiguous in permuted order) in
+// shared memory and every thread register-blocks kNearTPT targets against
+// broadcast shared-memory reads of the sources. FP64 throughout; the pair
+// loop is FP64-pipe bound.
+#include "device_math.cuh"
+#include "plan.hpp"
+
+namespace fktb {
+namespace {
+
+constexpr int kNearThreads = 128;
+constexpr int kNearTPT = 2;
+constexpr int kNearChunk = 512;  // sources staged per pass
+
+struct NearArgs {
+  int n, d, nrhs;
+  const double* pc;  // SoA permuted coordinates
+  const uint32_t* begin;
+  const uint32_t* end;
+  const FktbTile* tiles;
+  const uint32_t* nearPos;
+  const double* yp;  // permuted weights, n x nrhs
+  double* zp;        // permuted output, n x nrhs
+  FktbKernelDesc kd;
+};
+
+template <int KID, int D>
+__global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constant__ NearArgs A) {
+  constexpr int DD = D > 0 ? D : FKTB_MAX_DIM;
+  const int d = D > 0 ? D : A.d;
+  extern __shared__ double smem[];
+  double* sw = smem;                 // [kNearChunk]
+  double* sx = smem + kNearChunk;    // [d][kNearChunk]
+  const FktbTile tile = A.tiles[blockIdx.x];
+  const int leaf = tile.node;
+  const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
+  const int n = A.n;
+
+  int tpos[kNearTPT];
+  double tx[kNearTPT][DD];
+  double acc[kNearTPT];
+#pragma unroll
+  for (int i = 0; i < kNearTPT; ++i) {
+    const int idx = threadIdx.x + i * kNearThreads;
+    tpos[i] = idx < tile.count ? static_cast<int>(A.nearPos[tile.start + idx]) : -1;
+    const int p = tpos[i] >= 0 ? tpos[i] : 0;
+#pragma unroll
+    for (int a = 0; a < DD; ++a)
+      if (a < d) tx[i][a] = A.pc[static_cast<size_t>(a) * n + p];
+    acc[i] = 0.0;
+  }
+  for (int rhs = 0; rhs < A.nrhs; ++rhs) {
+    const double* y = A.yp + static_cast<size_t>(rhs) * n;
+    for (int cs = sb; cs < se; cs += kNearChunk) {
+      const int cn = min(kNearChunk, se - cs);
+      __syncthreads();
+      for (int s = threadIdx.x; s < cn; s += kNearThreads) {
+        sw[s] = y[cs + s];
+        for (int a = 0; a < d; ++a) sx[a * kNearChunk + s] = A.pc[static_cast<size_t>(a) * n + cs + s];
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int s = 0; s < cn; ++s) {
+        double sxa[DD];
+#pragma unroll
+        for (int a = 0; a < DD; ++a)
+          if (a < d) sxa[a] = sx[a * kNearChunk + s];
+        const double w = sw[s];
+#pragma unroll
+        for (int i = 0; i < kNearTPT; ++i) {
+          double dist2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < DD; ++a) {
+            if (a < d) {
+              const double t = tx[i][a] - sxa[a];
+              dist2 = fma(t, t, dist2);
+            }
+          }
+          double kv = kernel_value<KID>(A.kd, dist2);
+          kv = dist2 == 0.0 ? A.kd.diag : kv;
+          acc[i] = fma(kv, w, acc[i]);
+        }
+      }
+    }
+    double* z = A.zp + static_cast<size_t>(rhs) * n;
+#pragma unroll
+    for (int i = 0; i < kNearTPT; ++i) {
+      if (tpos[i] >= 0) atomicAdd(z + tpos[i], acc[i]);
+      acc[i] = 0.0;
+    }
+  }
+}
+
+template <int KID, int D>
+void launchNearT(const NearArgs& A, int tiles, cudaStream_t st) {
+  const int d = D > 0 ? D : A.d;
+  const size_t smem = static_cast<size_t>(kNearChunk) * (d + 1) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    FKTB_CUDA(cudaFuncSetAttribute(near_kernel<KID, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kNearChunk * (FKTB_MAX_DIM + 1) * sizeof(double))));
+    configured = true;
+  }
+  near_kernel<KID, D><<<tiles, kNearThreads, smem, st>>>(A);
+  FKTB_CUDA(cudaGetLastError());
+}
+
+template <int KID>
+void launchNearK(const NearArgs& A, int tiles, cudaStream_t st) {
+  switch (A.d) {
+    case 2: return launchNearT<KID, 2>(A, tiles, st);
+    case 3: return launchNearT<KID, 3>(A, tiles, st);
+    case 5: return launchNearT<KID, 5>(A, tiles, st);
+    default: return launchNearT<KID, 0>(A, tiles, st);
+  }
+}
+
+}  // namespace
+
+int nearTileSize() { return kNearThreads * kNearTPT; }
+
+void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
+  const int tiles = static_cast<int>(plan.nearTilesHost.size());
+  if (tiles == 0) return;
+  const DeviceTree& t = *plan.tree;
+  NearArgs A{t.n, t.d, nrhs, t.pc.get(), t.dBegin.get(), t.dEnd.get(), plan.dNearTiles.get(), t.dNearPos.get(), yp, zp, {}};
+  fillKernelDesc(plan.kernel, A.kd);
+  if (plan.options.hasDiagonal) A.kd.diag = plan.options.diagonal;
+  switch (plan.kernel.id) {
+    case FKTB_KERNEL_EXPONENTIAL: return launchNearK<FKTB_KERNEL_EXPONENTIAL>(A, tiles, st);
+    case FKTB_KERNEL_MATERN12: return launchNearK<FKTB_KERNEL_MATERN12>(A, tiles, st);
+    case FKTB_KERNEL_MATERN32: return launchNearK<FKTB_KERNEL_MATERN32>(A, tiles, st);
+    case FKTB_KERNEL_CAUCHY: return launchNearK<FKTB_KERNEL_CAUCHY>(A, tiles, st);
+    case FKTB_KERNEL_RATIONAL_QUADRATIC: return launchNearK<FKTB_KERNEL_RATIONAL_QUADRATIC>(A, tiles, st);
+    case FKTB_KERNEL_GAUSSIAN: return launchNearK<FKTB_KERNEL_GAUSSIAN>(A, tiles, st);
+    case FKTB_KERNEL_INVERSE_R: return launchNearK<FKTB_KERNEL_INVERSE_R>(A, tiles, st);
+    case FKTB_KERNEL_INVERSE_R2: return launchNearK<FKTB_KERNEL_INVERSE_R2>(A, tiles, st);
+    case FKTB_KERNEL_INVERSE_R3: return launchNearK<FKTB_KERNEL_INVERSE_R3>(A, tiles, st);
+    case FKTB_KERNEL_EXP_OVER_R: return launchNearK<FKTB_KERNEL_EXP_OVER_R>(A, tiles, st);
+    case FKTB_KERNEL_R_EXP: return launchNearK<FKTB_KERNEL_R_EXP>(A, tiles, st);
+    case FKTB_KERNEL_COS_OVER_R: return launchNearK<FKTB_KERNEL_COS_OVER_R>(A, tiles, st);
+    case FKTB_KERNEL_EXP_NEG_INV_R: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R>(A, tiles, st);
+    case FKTB_KERNEL_EXP_NEG_INV_R2: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R2>(A, tiles, st);
+  }
+  throw std::invalid_argument("near field: unknown kernel id");
+}
+
+}  // namespace fktb

@@ -1,0 +1,229 @@
+// Plan construction and the MVM pipeline (reference proj/src/transform.cpp:39-204).
+//
+// Plan: GPU tree (K1) -> GPU interaction sets (K2) -> exact tables on the host
+// (coefficients, harmonics, optional compression) -> kernel-parameter tables
+// and work tiles. Multiply: gather y into tree order -> S2M (K4) -> near (K3)
+// -> M2T (K5) -> scatter z back, all on one stream.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "device_math.cuh"
+#include "plan.hpp"
+
+namespace fktb {
+
+int nearTileSize();
+int farTileSize();
+int genericGMax();
+
+namespace {
+
+constexpr int kS2MTileSources = 4096;
+
+bool specialised(int d, int p) {
+  const int key = d * 100 + p;
+  return key == 206 || key == 304 || key == 306 || key == 308 || key == 504;
+}
+
+void buildFarParams(DevicePlan& plan) {
+  const int d = plan.d, p = plan.options.p;
+  const HarmonicStructure& hs = *plan.harmonics;
+  const CoefTable& table = coefTable(d, p);
+  auto fp = std::make_unique<FktbFarParams>();
+  std::memset(fp.get(), 0, sizeof(FktbFarParams));
+  fp->d = d;
+  fp->p = p;
+  fp->compressed = plan.compressed ? 1 : 0;
+  fillKernelDesc(plan.kernel, fp->kernel);
+  int cOff = 0, hOff = 0, tOff = 0, pref = 0;
+  for (int k = 0; k <= p; ++k) {
+    fp->hOff[k] = hOff;
+    fp->cOff[k] = cOff;
+    fp->tOff[k] = tOff;
+    const int hk = static_cast<int>(hs.degreeCount(k));
+    const int su = (p - k) / 2 + 1;
+    fp->slotsU[k] = su;
+    fp->slots[k] = plan.compressed ? plan.factors[static_cast<size_t>(k)].rank : su;
+    pref += hk * fp->slots[k];
+    hOff += hk;
+    cOff += hk * su;
+    tOff += su;
+  }
+  fp->hOff[p + 1] = hOff;
+  fp->cOff[p + 1] = cOff;
+  fp->tOff[p + 1] = tOff;
+  fp->P = cOff;
+  fp->H = hOff;
+  fp->Pref = pref;
+  // Radial table rows: Tbar_kjm * m!
+  int at = 0;
+  for (int k = 0; k <= p; ++k)
+    for (int s = 0; k + 2 * s <= p; ++s) {
+      const int j = k + 2 * s;
+      fp->tRow[fp->tOff[k] + s] = at;
+      double fact = 1.0;
+      for (int m = 1; m <= j; ++m) {
+        fact *= m;
+        if (at >= FKTB_TBAR_CAP) throw std::invalid_argument("expansion table exceeds the GPU parameter capacity");
+        fp->tb[at++] = table.tbarDouble(k, j, m) * fact;
+      }
+    }
+  if (plan.compressed) {
+    int f = 0, c = 0;
+    for (int k = 0; k <= p; ++k) {
+      fp->fOff[k] = f;
+      const RadialFactor& rf = plan.factors[static_cast<size_t>(k)];
+      for (int i = 0; i < rf.rank; ++i, ++f) {
+        if (f >= FKTB_FACTOR_MAX) throw std::invalid_argument("compression factors exceed the GPU parameter capacity");
+        const Laurent& F = rf.target[static_cast<size_t>(i)];
+        const Laurent& G = rf.source[static_cast<size_t>(i)];
+        fp->fLo[f] = F.minPower();
+        fp->fHi[f] = F.maxPower();
+        fp->fAt[f] = c;
+        for (int e = F.minPower(); e <= F.maxPower(); ++e) {
+          if (c >= FKTB_FACTOR_CAP) throw std::invalid_argument("compression factors exceed the GPU parameter capacity");
+          fp->fc[c++] = toDouble(F.coeff(e));
+        }
+        fp->gLo[f] = G.minPower();
+        fp->gHi[f] = G.maxPower();
+        fp->gAt[f] = c;
+        for (int e = G.minPower(); e <= G.maxPower(); ++e) {
+          if (c >= FKTB_FACTOR_CAP) throw std::invalid_argument("compression factors exceed the GPU parameter capacity");
+          fp->fc[c++] = toDouble(G.coeff(e));
+        }
+      }
+    }
+    fp->fOff[p + 1] = f;
+  }
+  plan.P = fp->P;
+  plan.H = fp->H;
+
+  // Per-harmonic fold Z_k * nrm_h^2 and the runtime chain table.
+  std::vector<double> hscale(static_cast<size_t>(fp->H));
+  const int L = d > 2 ? d - 2 : 0;
+  std::vector<int> cg(static_cast<size_t>(std::max(1, fp->H * L))), cc(static_cast<size_t>(fp->H)), ph(static_cast<size_t>(fp->H));
+  for (int k = 0; k <= p; ++k) {
+    int h = fp->hOff[k];
+    for (const HarmonicChain& ch : hs.chains(k)) {
+      hscale[static_cast<size_t>(h)] = hs.z(k) * ch.norm * ch.norm;
+      for (int l = 1; l <= L; ++l) cg[static_cast<size_t>(h * L + l - 1)] = g_index(p, l, ch.m[static_cast<size_t>(l)], ch.m[static_cast<size_t>(l - 1)] - ch.m[static_cast<size_t>(l)]);
+      cc[static_cast<size_t>(h)] = d == 2 ? k : ch.m[static_cast<size_t>(d - 2)];
+      ph[static_cast<size_t>(h)] = ch.phase;
+      ++h;
+    }
+  }
+  cudaStream_t st = plan.stream;
+  plan.dHScale.resize(hscale.size());
+  plan.dChainG.resize(cg.size());
+  plan.dChainC.resize(cc.size());
+  plan.dChainPh.resize(ph.size());
+  FKTB_CUDA(cudaMemcpyAsync(plan.dHScale.get(), hscale.data(), plan.dHScale.bytes(), cudaMemcpyHostToDevice, st));
+  FKTB_CUDA(cudaMemcpyAsync(plan.dChainG.get(), cg.data(), plan.dChainG.bytes(), cudaMemcpyHostToDevice, st));
+  FKTB_CUDA(cudaMemcpyAsync(plan.dChainC.get(), cc.data(), plan.dChainC.bytes(), cudaMemcpyHostToDevice, st));
+  FKTB_CUDA(cudaMemcpyAsync(plan.dChainPh.get(), ph.data(), plan.dChainPh.bytes(), cudaMemcpyHostToDevice, st));
+  plan.far = std::move(fp);
+}
+
+void buildTiles(DevicePlan& plan) {
+  const DeviceTree& t = *plan.tree;
+  const int ft = farTileSize(), nt = nearTileSize();
+  plan.farTilesHost.clear();
+  plan.nearTilesHost.clear();
+  plan.s2mTilesHost.clear();
+  for (int b = 0; b < t.nodes; ++b) {
+    const long long f0 = t.farOff[static_cast<size_t>(b)], f1 = t.farOff[static_cast<size_t>(b) + 1];
+    for (long long s = f0; s < f1; s += ft) plan.farTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(ft, f1 - s)), s});
+    if (f1 > f0)
+      for (long long s = t.begin[static_cast<size_t>(b)]; s < t.end[static_cast<size_t>(b)]; s += kS2MTileSources)
+        plan.s2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(kS2MTileSources, t.end[static_cast<size_t>(b)] - s)), s});
+    const long long n0 = t.nearOff[static_cast<size_t>(b)], n1 = t.nearOff[static_cast<size_t>(b) + 1];
+    for (long long s = n0; s < n1; s += nt) plan.nearTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(nt, n1 - s)), s});
+  }
+  auto upload = [&](DeviceBuffer<FktbTile>& dst, const std::vector<FktbTile>& src) {
+    dst.resize(std::max<size_t>(1, src.size()));
+    if (!src.empty())
+      FKTB_CUDA(cudaMemcpyAsync(dst.get(), src.data(), src.size() * sizeof(FktbTile), cudaMemcpyHostToDevice, plan.stream));
+  };
+  upload(plan.dFarTiles, plan.farTilesHost);
+  upload(plan.dNearTiles, plan.nearTilesHost);
+  upload(plan.dS2mTiles, plan.s2mTilesHost);
+}
+
+void ensureWorkspace(DevicePlan& plan, int nrhs) {
+  if (nrhs <= plan.nrhsCap) return;
+  const size_t n = static_cast<size_t>(plan.n);
+  plan.dYp.resize(n * nrhs);
+  plan.dZp.resize(n * nrhs);
+  plan.dMoments.resize(std::max<size_t>(1, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs));
+  plan.nrhsCap = nrhs;
+}
+
+}  // namespace
+
+std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
+                                       const PlanOptions& options) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto plan = std::make_unique<DevicePlan>();
+  plan->n = n;
+  plan->d = d;
+  plan->options = options;
+  plan->kernel = kernel;
+  if (options.barnesHut) throw std::invalid_argument("unsupported on the GPU path: Barnes-Hut plans (SURVEY §8f 'next')");
+  // Validation order follows the reference constructor (transform.cpp:39-80).
+  if (options.leafCapacity < 1) throw std::invalid_argument("leaf capacity must be >= 1");
+  if (n < 1) throw std::invalid_argument("point cloud must be nonempty");
+  if (options.p < 0) throw std::invalid_argument("plan requires p >= 0");
+  if (!(options.theta > 0.0 && options.theta < 1.0)) throw std::invalid_argument("theta must be in (0, 1)");
+  if (d < 2) throw std::invalid_argument("HarmonicBasis requires d >= 2");
+  const CoefTable& table = coefTable(d, options.p);  // OrderTooLarge for p > 20
+  bool compress = false;
+  if (options.compression == 0)
+    compress = kernel.recurrence.has_value();
+  else if (options.compression == 1) {
+    if (!kernel.recurrence) throw NotRecurrenceKernelError(kernel.name);
+    compress = true;
+  }
+  if (!specialised(d, options.p) && (d - 2) * (options.p + 1) * (options.p + 2) / 2 > genericGMax())
+    throw std::invalid_argument("unsupported on the GPU path: (d, p) too large for the runtime far-field kernels");
+
+  FKTB_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+  plan->tree = std::make_unique<DeviceTree>();
+  buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
+  computeSetsGpu(*plan->tree, options.theta);
+
+  plan->harmonics = std::make_unique<HarmonicStructure>(d, options.p);
+  if (compress) plan->factors = radialCompression(kernel, table, options.p);
+  plan->compressed = compress;
+  buildFarParams(*plan);
+  buildTiles(*plan);
+  plan->dX.resize(static_cast<size_t>(n) * d);
+  FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
+  ensureWorkspace(*plan, 1);
+  FKTB_CUDA(cudaStreamSynchronize(plan->stream));
+  plan->planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return plan;
+}
+
+void destroyPlan(DevicePlan* plan) {
+  if (!plan) return;
+  if (plan->stream) cudaStreamSynchronize(plan->stream);
+  cudaStream_t st = plan->stream;
+  delete plan;
+  if (st) cudaStreamDestroy(st);
+}
+
+void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
+  ensureWorkspace(plan, nrhs);
+  const size_t n = static_cast<size_t>(plan.n);
+  launchGatherY(plan, y, plan.dYp.get(), nrhs, st);
+  FKTB_CUDA(cudaMemsetAsync(plan.dZp.get(), 0, n * nrhs * sizeof(double), st));
+  FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double), st));
+  launchS2M(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, st);
+  launchNear(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
+  launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, st);
+  launchScatterZ(plan, plan.dZp.get(), z, nrhs, st);
+}
+
+}  // namespace fktb

@@ -1,0 +1,157 @@
+// Host-side plan structures (product code). A DeviceTree owns the GPU copy of
+// the partition tree and its interaction sets; a DevicePlan adds the
+// expansion tables and the MVM workspaces. See DESIGN.md §2 for the HBM
+// layout.
+#ifndef FKTB_PLAN_HPP
+#define FKTB_PLAN_HPP
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "fkt_device_types.h"
+#include "tables.hpp"
+
+namespace fktb {
+
+template <class T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t n) { resize(n); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  void resize(std::size_t n) {
+    release();
+    if (n) FKTB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+  std::size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// Partition tree + interaction sets resident in HBM.
+struct DeviceTree {
+  int n = 0, d = 0, leafCapacity = 0;
+  double theta = 0.0;
+  bool hasSets = false;
+  int depth = 0;
+
+  // Device: permuted coordinates SoA (pc[a*n + pos]), permutation pos->orig.
+  DeviceBuffer<double> pc;
+  DeviceBuffer<uint32_t> order;
+
+  // Host node arrays in reference pre-order numbering (tree.cpp:41-171).
+  int nodes = 0;
+  std::vector<uint32_t> begin, end;
+  std::vector<int> left, right;
+  std::vector<double> boxLo, boxHi, center, radius;  // d per node for box/center
+
+  // Device node arrays (pre-order).
+  DeviceBuffer<double> dCenter, dLimit2;
+  DeviceBuffer<int> dLeft, dRight;
+  DeviceBuffer<uint32_t> dBegin, dEnd;
+
+  // Interaction sets as node-major CSR over PERMUTED positions, ascending
+  // (tree.cpp:173-213 restated point-wise on the GPU).
+  long long farTotal = 0, nearTotal = 0;
+  std::vector<long long> farOff, nearOff;  // host copies, nodes + 1
+  DeviceBuffer<long long> dFarOff, dNearOff;
+  DeviceBuffer<uint32_t> dFarPos, dNearPos;
+
+  cudaStream_t stream = nullptr;
+};
+
+// Build the tree for `x` (row-major n x d, host) on `stream`.
+void buildTreeGpu(DeviceTree& t, const double* hostX, int n, int d, int leafCapacity, cudaStream_t stream);
+void computeSetsGpu(DeviceTree& t, double theta);
+
+// Host materialisation of the sets in the reference's form: original point
+// indices, ascending per node.
+void materializeSets(const DeviceTree& t, bool far, std::vector<long long>& off, std::vector<uint32_t>& idx);
+
+// ---------------------------------------------------------------------------
+struct PlanOptions {
+  int p = 4;
+  double theta = 0.75;
+  int leafCapacity = 512;
+  int compression = 0;  // 0 auto, 1 on, 2 off
+  bool eagerOperators = true;
+  bool barnesHut = false;
+  int threads = 0;
+  bool hasDiagonal = false;
+  double diagonal = 0.0;
+};
+
+struct DevicePlan {
+  int n = 0, d = 0;
+  PlanOptions options;
+  KernelSpec kernel;
+  std::unique_ptr<DeviceTree> tree;
+  bool compressed = false;
+  std::vector<RadialFactor> factors;
+  std::unique_ptr<HarmonicStructure> harmonics;
+  int P = 0, H = 0;
+
+  std::unique_ptr<FktbFarParams> far;   // kernel-parameter tables
+  DeviceBuffer<double> dHScale;          // per harmonic: Z_k * norm_h^2
+  DeviceBuffer<int> dChainG, dChainC, dChainPh;  // generic runtime chain table
+  std::vector<FktbTile> farTilesHost, nearTilesHost, s2mTilesHost;
+  DeviceBuffer<FktbTile> dFarTiles, dNearTiles, dS2mTiles;
+  DeviceBuffer<double> dMoments;         // nodes x P x nrhsCap
+  DeviceBuffer<double> dX;               // original coordinates, row-major (dense paths)
+  DeviceBuffer<double> dYp, dZp;         // permuted workspaces (n x nrhsCap)
+  DeviceBuffer<double> dYio, dZio;       // staging for host-buffer multiplies
+  int nrhsCap = 0;
+  double planSeconds = 0.0;
+  std::mutex mutex;                       // multiply() is serialised per plan
+  cudaStream_t stream = nullptr;
+};
+
+std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
+                                       const PlanOptions& options);
+void destroyPlan(DevicePlan* plan);
+// z = K y for nrhs column-major right-hand sides; y, z device pointers.
+void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
+
+// Kernel launchers (near.cu, far.cu, dense.cu).
+void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+void launchS2M(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
+void launchM2T(const DevicePlan& plan, const double* moments, double* zp, int nrhs, cudaStream_t stream);
+void launchGatherY(const DevicePlan& plan, const double* y, double* yp, int nrhs, cudaStream_t stream);
+void launchScatterZ(const DevicePlan& plan, const double* zp, double* z, int nrhs, cudaStream_t stream);
+void denseRowsGpu(int n, int d, const double* dX, const FktbKernelDesc& kd, const double* dY, int m,
+                  const int64_t* dRows, double* dZ, cudaStream_t stream);
+
+}  // namespace fktb
+
+#endif
