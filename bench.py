@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""FKT MVM benchmark — BASELINE.json metric on the headline config (cfg2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--cfg C]
+
+Our arm: one B200-native FKT plan per rank (cfg2: Matern-3/2 l=0.1, N=1e6,
+d=3, p=6, leaf 512, theta 0.5, SURVEY Appendix B inputs from fkt::Rng(42)).
+`value` = whole-job MVMs/s with y and z resident in HBM (CUDA events around
+K back-to-back device multiplies on the launching stream, max over ranks);
+`e2e` = the same through the C-ABI host-buffer call (pinned host y -> H2D ->
+MVM -> D2H z every step). The roofline is for the dominant kernel (near
+field K3, FP64-pipe bound) against the FP64 FMA peak measured live on this
+GPU. The reference arm times the unmodified reference FKT (oracle/_ref) on
+the host cores. Multi-GPU: independent replicas per rank ("replicas only",
+DESIGN.md §6), scaling "weak".
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FKT MVMs/sec (and effective interactions/sec) at N=1e6 d=3, % of roofline"
+
+CONFIGS = {
+    1: dict(kernel="cauchy", params={"sigma": 1.0}, n=20000, p=4, leaf=512, theta=0.5, d=3, nrhs=1),
+    2: dict(kernel="matern32", params={"sigma": 1.0, "rho": 0.1}, n=1000000, p=6, leaf=512, theta=0.5, d=3, nrhs=1),
+    3: dict(kernel="gaussian", params={}, n=1000000, p=4, leaf=1024, theta=0.75, d=5, nrhs=1),
+    4: dict(kernel="inverse-r", params={}, n=4000000, p=8, leaf=512, theta=0.5, d=3, nrhs=1),
+    5: dict(kernel="cauchy", params={"sigma": 1.0}, n=2000000, p=6, leaf=512, theta=0.75, d=2, nrhs=16),
+}
+
+# BASELINE.md §3 flop convention: +,-,x = 1, FMA = 2, div/sqrt/rsqrt = 8, exp = 20.
+def near_flops_per_pair(kernel: str, d: int) -> int:
+    diff = 3 * d - 1  # d subtractions, d squares, d-1 adds
+    extra = {
+        "cauchy": 1 + 1 + 8 + 2, "rational-quadratic": 1 + 1 + 8 + 2, "gaussian": 20 + 2,
+        "inverse-r": 8 + 2, "inverse-r2": 8 + 2, "matern32": 8 + 1 + 1 + 20 + 1 + 1 + 2,
+        "matern12": 8 + 8 + 20 + 1 + 2, "exponential": 8 + 20 + 2,
+    }.get(kernel, 8 + 20 + 2)
+    return diff + extra
+
+
+def workload_desc(cfg):
+    c = CONFIGS[cfg]
+    return (f"cfg{cfg}: {c['kernel']} {c['params']} N={c['n']} d={c['d']} p={c['p']} leaf={c['leaf']} "
+            f"theta={c['theta']} nrhs={c['nrhs']}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def near_evals(tree) -> int:
+    off, _ = tree.nearCsr()
+    counts = np.diff(off)
+    sizes = tree.ends.astype(np.int64) - tree.begins.astype(np.int64)
+    return int(np.sum(counts * sizes))
+
+
+def s2m_pairs(tree) -> int:
+    off, _ = tree.farCsr()
+    has = np.diff(off) > 0
+    sizes = tree.ends.astype(np.int64) - tree.begins.astype(np.int64)
+    return int(np.sum(sizes[has]))
+
+
+def golden_parity(cfg, z):
+    path = os.path.join(ROOT, "tests", "golden", f"cfg{cfg}_ref.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    rows = g["rows"]
+    zr = g["z_rows"]
+    zz = z[rows] if z.ndim == 1 else z[rows, :]
+    out = {"rows": int(rows.size), "rel_l2_vs_reference_fkt": float(np.linalg.norm(zz - zr) / np.linalg.norm(zr))}
+    zc = zz if zz.ndim == 1 else zz[:, 0]
+    out["rel_l2_vs_dense"] = float(np.linalg.norm(zc - g["dense_rows"]) / np.linalg.norm(g["dense_rows"]))
+    return out
+
+
+def traffic_for(cfg):
+    path = os.path.join(ROOT, "profiles", "near_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"cfg{cfg}")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_04487_b200 as fkt
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.cfg]
+    n, nrhs = c["n"], c["nrhs"]
+    x, w = fkt.synthConfig(args.cfg, n)
+    t0 = time.perf_counter()
+    pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(c["kernel"], c["params"]),
+                  fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"]))
+    plan_s = time.perf_counter() - t0
+    info = pl.info()
+    wcols = w.reshape(n, nrhs) if nrhs > 1 else w
+    ydev = torch.from_numpy(np.ascontiguousarray(wcols.T if nrhs > 1 else wcols)).cuda()
+    zdev = torch.empty_like(ydev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        pl.multiply_device(ydev, zdev, stream=stream)
+    torch.cuda.synchronize()
+    zhost = zdev.cpu().numpy()
+    parity = golden_parity(args.cfg, zhost.T if nrhs > 1 else zhost) if rank == 0 else None
+
+    # ---- timed region: K device multiplies -------------------------------
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            pl.multiply_device(ydev, zdev, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-stage timing (same stream) for the roofline ------------------
+    stage_ms = np.zeros(5)
+    reps = max(3, min(args.steps, 20))
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        ev[0].record(stream)
+        for s in range(5):
+            pl.stage_device(s, ydev, zdev, nrhs=nrhs, stream=stream)
+            ev[s + 1].record(stream)
+        torch.cuda.synchronize()
+        stage_ms += np.array([ev[s].elapsed_time(ev[s + 1]) for s in range(5)])
+    stage_ms /= reps
+
+    # ---- e2e: public host-buffer API, pinned buffers, H2D + D2H per step ---
+    yh = torch.from_numpy(np.asfortranarray(wcols)).pin_memory() if nrhs == 1 else \
+        torch.from_numpy(np.ascontiguousarray(wcols.T)).pin_memory()
+    zh = torch.empty_like(yh).pin_memory()
+    import ctypes as C
+
+    def host_mul():
+        rc = fkt.lib.fkt_plan_multiply(pl._h, C.cast(C.c_void_p(yh.data_ptr()), C.POINTER(C.c_double)),
+                                       C.cast(C.c_void_p(zh.data_ptr()), C.POINTER(C.c_double)), nrhs)
+        fkt._check(rc)
+
+    for _ in range(max(1, args.warmup // 2)):
+        host_mul()
+    if world > 1:
+        dist.barrier()
+    te = time.perf_counter()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(e2e_steps):
+        host_mul()
+    e2e_s = (time.perf_counter() - te) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- roofline (dominant kernel: near field) ---------------------------
+    peak = C.c_double()
+    fkt._check(fkt.lib.fkt_fma_peak(0, C.byref(peak)))
+    peak_tf = peak.value / 1e12
+    tree = pl.tree()
+    nev = near_evals(tree)
+    fpp = near_flops_per_pair(c["kernel"], c["d"]) + 2 * (nrhs - 1)
+    near_flops = nev * fpp
+    P = info["coefficient_count"]
+    far_pairs = info["far_total"] + s2m_pairs(tree)
+    far_flops = far_pairs * (2 * P + 2 * P * nrhs)
+    near_ms = stage_ms[2]
+    achieved = near_flops / (near_ms * 1e-3) / 1e12
+    mvm_s = ms * 1e-3
+    value = world * 1.0 / mvm_s
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "MVM/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY Appendix B recipe, fkt::Rng(42); no public dataset)",
+        "config": {
+            "workload": workload_desc(args.cfg),
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2: far lists %.0f MB + near lists %.0f MB + coordinates %.0f MB per step"
+                  % (info["far_total"] * 4 / 1e6, info["near_total"] * 4 / 1e6, n * c["d"] * 8 / 1e6),
+            "plan_seconds": plan_s,
+            "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
+            "near_evals": nev, "coefficients": P,
+        },
+        "effective_interactions_per_s": world * float(n) * n * nrhs / mvm_s,
+        "stage_ms": {"gather": stage_ms[0], "s2m": stage_ms[1], "near": stage_ms[2], "m2t": stage_ms[3],
+                     "scatter": stage_ms[4]},
+        "roofline": {
+            "kernel": "near_kernel (K3)",
+            "bound": "fp64",
+            "achieved": achieved,
+            "peak": peak_tf,
+            "peak_source": "fp64 FMA-chain microbenchmark measured live in this run (fkt_fma_peak); "
+                           "MEASURED_PEAKS.json has no fp64 entry",
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_tf,
+            "traffic": traffic_for(args.cfg),
+            "flops_per_launch": near_flops,
+            "flops_per_pair": fpp,
+            "whole_step_frac": (near_flops + far_flops) / mvm_s / 1e12 / peak_tf,
+        },
+        "e2e": {"value": world * 1.0 / e2e_s, "unit": "MVM/s", "h2d_bytes_per_step": int(yh.numel() * 8),
+                "d2h_bytes_per_step": int(zh.numel() * 8),
+                "method": "fkt_plan_multiply (C-ABI, pinned host y/z, H2D+MVM+D2H per step), wall clock"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks.summary(),
+        "parity": parity,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cfg, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def _ref_sample_run(cfg, n_s, reps, warmup):
+    """Reference FKT (oracle/_ref) on the cfg recipe with n_s points; returns seconds per MVM."""
+    from oracle import ref
+
+    c = CONFIGS[cfg]
+    x, w = ref.gen_config(cfg, n_s)
+    rp = ref.RefPlan(x, c["kernel"], c["params"], p=c["p"], theta=c["theta"], leaf=c["leaf"], eager=False,
+                     threads=0)
+    for _ in range(warmup):
+        rp.multiply(w)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        rp.multiply(w)
+        ts.append(time.perf_counter() - t0)
+    return ts, rp.plan_seconds
+
+
+def cpu_baseline(cfg, budget_s=30.0):
+    """Reference CPU FKT on the host cores, bounded sample (10-30 s of CPU work)."""
+    c = CONFIGS[cfg]
+    cores = os.cpu_count()
+    n_probe = min(c["n"], 100000)
+    ts, _ = _ref_sample_run(cfg, n_probe, 1, 0)
+    t_full_est = ts[0] * c["n"] / n_probe
+    if t_full_est <= budget_s:
+        ts, plan_s = _ref_sample_run(cfg, c["n"], 1, 0)
+        t, n_s = ts[0], c["n"]
+        sample = f"one full reference MVM at N={c['n']} (streaming, {cores} threads)"
+    else:
+        n_s = int(min(c["n"], max(20000, c["n"] * budget_s / t_full_est)))
+        ts, plan_s = _ref_sample_run(cfg, n_s, 1, 0)
+        t = ts[0] * c["n"] / n_s
+        sample = (f"reference MVM on the first {n_s} points of the cfg{cfg} recipe (streaming, {cores} threads), "
+                  f"{ts[0]:.2f} s, scaled linearly to N={c['n']}")
+    return {"value": 1.0 / t, "unit": "MVM/s", "cores": cores, "kind": "reference", "sample": sample,
+            "seconds_per_mvm": t}
+
+
+def run_reference(args):
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return
+    from oracle import ref
+
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfktref.so not built"}))
+        return
+    c = CONFIGS[args.cfg]
+    cores = os.cpu_count()
+    # Size each step so warmup + steps stays within a few minutes.
+    n_probe = min(c["n"], 100000)
+    ts, _ = _ref_sample_run(args.cfg, n_probe, 1, 0)
+    per_full = ts[0] * c["n"] / n_probe
+    budget = args.ref_budget
+    total_steps = args.steps + args.warmup
+    n_s = c["n"] if per_full * total_steps <= budget else int(max(20000, c["n"] * budget / (per_full * total_steps)))
+    n_s = min(n_s, c["n"])
+    ts, plan_s = _ref_sample_run(args.cfg, n_s, args.steps, args.warmup)
+    t_step = float(np.mean(ts))
+    t_scaled = t_step * c["n"] / n_s
+    value = 1.0 / t_scaled
+    sample = (f"each step = one reference FKT MVM (streaming, {cores} threads) on "
+              + (f"the full N={c['n']}" if n_s == c["n"] else
+                 f"the first {n_s} points of the cfg{args.cfg} recipe, time scaled linearly to N={c['n']}"))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MVM/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_scaled * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY Appendix B recipe, fkt::Rng(42))",
+        "config": {"workload": workload_desc(args.cfg), "parallelism": "host cores", "sample_n": n_s,
+                   "reference_plan_seconds": plan_s},
+        "cpu_baseline": {"value": value, "unit": "MVM/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "MVM/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "effective_interactions_per_s": float(c["n"]) * c["n"] * c["nrhs"] / t_scaled,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

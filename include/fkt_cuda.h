@@ -150,6 +150,11 @@ int fkt_compression_ranks(const char* kernel, const char* const* keys, const dou
 double fkt_addition_normalizer(int d, int k);
 long long fkt_harmonic_count(int d, int k);
 
+/* Measurement support: FMA-pipe peak (FLOP/s, FMA = 2) of the current device,
+ * fp64 (fp32 = 0) or fp32 (fp32 = 1): the roofline denominator for the
+ * FP64-bound kernels. */
+int fkt_fma_peak(int fp32, double* flops_per_s);
+
 /* Seeded synthetic inputs (reference fkt::Rng, synthetic.hpp:17-50;
  * generators synthetic.cpp:7-55). kind: "cube", "sphere", "mixture".
  * y (optional) receives normalVector(n) drawn after the cloud. */

@@ -406,9 +406,44 @@ constexpr ChainTable<D, P> make_chain_table() {
 // scale, the direction is taken). For x = 0 every degree >= 1 vanishes and
 // Yraw[0] = 1, which is the collocated-source rule of
 // proj/src/expansion.cpp:273-289 once the norm is folded in.
+// Number of chains in levels LEVEL..D-2 below m_{LEVEL-1} = mPrev.
+constexpr int chain_count(int d, int level, int mPrev) {
+  if (level == d - 2) return 2 * mPrev + 1;
+  int c = 0;
+  for (int m = 0; m <= mPrev; ++m) c += chain_count(d, level + 1, m);
+  return c;
+}
+
+// Chain products for levels LEVEL..D-2 below a fixed prefix, generated by
+// template recursion (nested ascending loops, the last level emitting +m then
+// -m: the order of proj/src/harmonics.cpp:62-103). Every index is a template
+// constant, so g/cA/cB/Y stay in registers.
+template <int D, int P, int LEVEL, int MPREV, int M, int H0>
+__device__ __forceinline__ void chain_products(double prod, const double* g, const double* cA, const double* cB,
+                                               double* Y) {
+  if constexpr (M <= MPREV) {
+    const double pr = prod * g[g_index(P, LEVEL, M, MPREV - M)];
+    if constexpr (LEVEL == D - 2) {
+      Y[H0] = pr * cA[M];
+      if constexpr (M > 0) Y[H0 + 1] = pr * cB[M];
+      chain_products<D, P, LEVEL, MPREV, M + 1, H0 + (M > 0 ? 2 : 1)>(prod, g, cA, cB, Y);
+    } else {
+      chain_products<D, P, LEVEL + 1, M, 0, H0>(pr, g, cA, cB, Y);
+      chain_products<D, P, LEVEL, MPREV, M + 1, H0 + chain_count(D, LEVEL + 1, M)>(prod, g, cA, cB, Y);
+    }
+  }
+}
+
+template <int D, int P, int K>
+__device__ __forceinline__ void chain_degrees(const double* g, const double* cA, const double* cB, double* Y) {
+  if constexpr (K <= P) {
+    chain_products<D, P, 1, K, 0, harmonic_offset(D, K)>(1.0, g, cA, cB, Y);
+    chain_degrees<D, P, K + 1>(g, cA, cB, Y);
+  }
+}
+
 template <int D, int P>
 __device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, double (&Y)[ChainTable<D, P>::H]) {
-  constexpr ChainTable<D, P> T = make_chain_table<D, P>();
   const double inv = r > 0.0 ? 1.0 / r : 0.0;
   double v[D];
 #pragma unroll
@@ -423,8 +458,12 @@ __device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, do
     cB[m] = cB[m - 1] * cx + cA[m - 1] * cy;
   }
   if constexpr (D == 2) {
+    Y[0] = 1.0;
 #pragma unroll
-    for (int h = 0; h < T.H; ++h) Y[h] = T.ph[h] >= 0 ? cA[T.ci[h]] : cB[T.ci[h]];
+    for (int k = 1; k <= P; ++k) {
+      Y[2 * k - 1] = cA[k];
+      Y[2 * k] = cB[k];
+    }
   } else {
     double tail[D - 1];
     {
@@ -453,13 +492,7 @@ __device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, do
                    (1.0 / n);
       }
     }
-#pragma unroll
-    for (int h = 0; h < T.H; ++h) {
-      double prod = T.ph[h] >= 0 ? cA[T.ci[h]] : cB[T.ci[h]];
-#pragma unroll
-      for (int l = 0; l < D - 2; ++l) prod *= g[T.gi[h][l]];
-      Y[h] = prod;
-    }
+    chain_degrees<D, P, 0>(g, cA, cB, Y);
   }
 }
 

@@ -1,4 +1,5 @@
-nvidia-smi --query-gpu=name,clocks.max.sm --format=csv
-python -c "import paper_2106_04487_b200 as f; print(f.lib.fkt_version())"
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "cfg1" 2>&1 | tail -30
-timeout 900 python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -40
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -5
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -2 gpurun_out/bench2.err
+python -c "
+import json; d=json.load(open('gpurun_out/bench2.json'))
+print(d['value'], d['ms_per_step'], d['stage_ms'], d['roofline']['frac'], d['parity'])"
