@@ -1,0 +1,85 @@
+// FP64 elementary functions for the near-field pair loop (sm_100a).
+//
+// The pair loop is bound by FP64-pipe issue, so these trade the last bits of
+// libm's correctly rounded results for fewer instructions while keeping a
+// relative error <= ~5e-14 per evaluation (z is gated at rel-L2 1e-10):
+//   * exp_neg(u) = e^-u, u >= 0: 64-entry 2^(j/64) table in shared memory,
+//     two-step Cody-Waite reduction, degree-4 Taylor polynomial (|f| <=
+//     ln2/128), exponent added in the integer pipe. 9 FP64 ops.
+//   * rsqrt_nr / sqrt_nr: MUFU rsqrt.approx.f64 + one Newton step. 4 FP64 ops.
+//   * rcp_nr: MUFU rcp.approx.f64 + one Newton step. 2 FP64 ops.
+#ifndef FKTB_FASTMATH_CUH
+#define FKTB_FASTMATH_CUH
+
+#include <cstdint>
+
+namespace fktb {
+
+constexpr int kExpTable = 64;
+// Added to every squared pair distance: keeps rsqrt finite at r == 0 and is
+// below one ulp of any squared distance >= 1e-284.
+constexpr double kQBias = 1e-300;
+
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// 1/sqrt(x), x > 0.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  const double y0 = rsqrt_approx(x);
+  const double h = x * y0;
+  const double e = fma(-h, y0, 1.0);
+  return fma(0.5 * y0, e, y0);
+}
+
+// sqrt(x) for x > 0 (callers bias squared distances by kQBias so x == 0
+// never reaches the approximation's infinity).
+__device__ __forceinline__ double sqrt_nr(double x) {
+  const double y0 = rsqrt_approx(x);
+  const double h = x * y0;
+  const double e = fma(-h, y0, 1.0);
+  return fma(0.5 * h, e, h);
+}
+
+// 1/x, x normal.
+__device__ __forceinline__ double rcp_nr(double x) {
+  const double y0 = rcp_approx(x);
+  const double e = fma(-x, y0, 1.0);
+  return fma(y0, e, y0);
+}
+
+// e^-u for u >= 0 (underflows to ~0 past u = 708). tab: 2^(j/64), j < 64.
+__device__ __forceinline__ double exp_neg(double u, const double* __restrict__ tab) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr double kInvStep = 92.332482616893656;  // 64 / ln 2
+  constexpr double kStepHi = 0.010830424696223417;  // ln2/64, high part (exact multiple product)
+  constexpr double kStepLo = 2.572804622327669e-14;  // ln2/64 - kStepHi
+  // clamp u <= ~708 on the high word (integer pipe): e^-708 ~ 3e-308, and
+  // keeps the exponent arithmetic below in the normal range
+  u = __hiloint2double(min(__double2hiint(u), 0x40862000), __double2loint(u));
+  const double t = fma(-u, kInvStep, kMagic);
+  const int k = __double2loint(t);  // round(-u * 64 / ln2), <= 0
+  const double kd = t - kMagic;
+  double f = fma(kd, -kStepHi, -u);
+  f = fma(kd, -kStepLo, f);
+  double p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(f, p, 0.5);
+  p = fma(f, p, 1.0);
+  p = fma(f, p, 1.0);
+  const double tj = tab[k & (kExpTable - 1)];
+  const int e = k >> 6;  // arithmetic shift: floor(k / 64)
+  const double scaled = __hiloint2double(__double2hiint(tj) + (e << 20), __double2loint(tj));
+  return scaled * p;
+}
+
+}  // namespace fktb
+
+#endif

@@ -8,7 +8,11 @@
 // broadcast shared-memory reads of the sources. FP64 throughout; the pair
 // loop is FP64-pipe bound.
 #include "device_math.cuh"
+#include "fastmath.cuh"
 #include "plan.hpp"
+
+#include <cmath>
+#include <mutex>
 
 namespace fktb {
 namespace {
@@ -96,6 +100,165 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for the hot kernels in d = 2, 3, 5: coordinates pre-scaled by the
+// kernel length scale (and weights by its prefactor) so the pair body is the
+// canonical kernel; FP64 fast math (fastmath.cuh); 4 targets per thread
+// against AoS shared-memory sources read with 128-bit broadcast loads.
+constexpr int kFastThreads = 64;
+constexpr int kFastTPT = 4;  // kFastThreads * kFastTPT == tile size
+static_assert(kFastThreads * kFastTPT == kNearThreads * kNearTPT, "near tile size");
+
+template <int KID>
+struct FastKernel {
+  static constexpr bool supported =
+      KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
+      KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN ||
+      KID == FKTB_KERNEL_INVERSE_R || KID == FKTB_KERNEL_INVERSE_R2;
+  static constexpr bool needsTable =
+      KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
+      KID == FKTB_KERNEL_GAUSSIAN;
+  // canonical K at scaled squared distance q (> 0 unless the select handles 0)
+  __device__ static __forceinline__ double eval(double q, const double* tab) {
+    if constexpr (KID == FKTB_KERNEL_MATERN32) {
+      const double u = sqrt_nr(q);
+      const double e = exp_neg(u, tab);
+      return fma(u, e, e);
+    } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
+      return exp_neg(sqrt_nr(q), tab);
+    } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
+      return rcp_nr(1.0 + q);
+    } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
+      return rsqrt_nr(1.0 + q);
+    } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
+      return exp_neg(q, tab);
+    } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
+      return rsqrt_nr(q);
+    } else {
+      return rcp_nr(q);
+    }
+  }
+};
+
+// (scale for coordinates, prefactor for weights)
+inline void fastScales(const FktbKernelDesc& k, double& sc, double& wf) {
+  sc = 1.0;
+  wf = 1.0;
+  switch (k.id) {
+    case FKTB_KERNEL_MATERN32: sc = k.a; wf = k.s2; break;
+    case FKTB_KERNEL_MATERN12: sc = 1.0 / k.rho; wf = k.s2; break;
+    case FKTB_KERNEL_CAUCHY:
+    case FKTB_KERNEL_RATIONAL_QUADRATIC: sc = std::sqrt(k.is2); break;
+    default: break;
+  }
+}
+
+struct FastArgs {
+  NearArgs a;
+  double sc, wf;
+  double diagCanon;  // diag / wf
+  int sel;           // apply the r == 0 convention explicitly
+  const double* expTable;
+};
+
+template <int KID, int D, bool SEL>
+__global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant__ FastArgs F) {
+  constexpr int SP = (D + 2) / 2 * 2;  // AoS stride (coords + weight), even
+  __shared__ __align__(16) double ss[kNearChunk * SP];
+  __shared__ double tab[kExpTable];
+  const NearArgs& A = F.a;
+  if constexpr (FastKernel<KID>::needsTable)
+    for (int i = threadIdx.x; i < kExpTable; i += kFastThreads) tab[i] = F.expTable[i];
+  const FktbTile tile = A.tiles[blockIdx.x];
+  const int leaf = tile.node;
+  const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
+  const int n = A.n;
+  int tpos[kFastTPT];
+  double tx[kFastTPT][D];
+  double acc[kFastTPT];
+#pragma unroll
+  for (int i = 0; i < kFastTPT; ++i) {
+    const int idx = threadIdx.x + i * kFastThreads;
+    tpos[i] = idx < tile.count ? static_cast<int>(A.nearPos[tile.start + idx]) : -1;
+    const int p = tpos[i] >= 0 ? tpos[i] : 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) tx[i][a] = A.pc[static_cast<size_t>(a) * n + p] * F.sc;
+    acc[i] = 0.0;
+  }
+  for (int rhs = 0; rhs < A.nrhs; ++rhs) {
+    const double* y = A.yp + static_cast<size_t>(rhs) * n;
+    for (int cs = sb; cs < se; cs += kNearChunk) {
+      const int cn = min(kNearChunk, se - cs);
+      __syncthreads();
+      for (int s = threadIdx.x; s < cn; s += kFastThreads) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) ss[s * SP + a] = A.pc[static_cast<size_t>(a) * n + cs + s] * F.sc;
+        ss[s * SP + D] = y[cs + s] * F.wf;
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int s = 0; s < cn; ++s) {
+        double src[SP];
+#pragma unroll
+        for (int q = 0; q < SP; q += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(&ss[s * SP + q]);
+          src[q] = v.x;
+          src[q + 1] = v.y;
+        }
+        const double w = src[D];
+#pragma unroll
+        for (int i = 0; i < kFastTPT; ++i) {
+          const double d0 = tx[i][0] - src[0];
+          double q = fma(d0, d0, kQBias);
+#pragma unroll
+          for (int a = 1; a < D; ++a) {
+            const double da = tx[i][a] - src[a];
+            q = fma(da, da, q);
+          }
+          double kv = FastKernel<KID>::eval(q, tab);
+          if constexpr (SEL) kv = q == kQBias ? F.diagCanon : kv;
+          acc[i] = fma(kv, w, acc[i]);
+        }
+      }
+    }
+    double* z = A.zp + static_cast<size_t>(rhs) * n;
+#pragma unroll
+    for (int i = 0; i < kFastTPT; ++i) {
+      if (tpos[i] >= 0) atomicAdd(z + tpos[i], acc[i]);
+      acc[i] = 0.0;
+    }
+  }
+}
+
+// 2^(j/64), j < 64, correctly rounded (host long double).
+const double* expTableDevice() {
+  static double* dev = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    double host[kExpTable];
+    for (int j = 0; j < kExpTable; ++j) host[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / kExpTable));
+    FKTB_CUDA(cudaMalloc(&dev, sizeof(host)));
+    FKTB_CUDA(cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice));
+  });
+  return dev;
+}
+
+template <int KID, int D>
+void launchFastT(const NearArgs& A, int tiles, cudaStream_t st) {
+  FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice()};
+  fastScales(A.kd, F.sc, F.wf);
+  F.diagCanon = A.kd.diag / F.wf;
+  // The canonical formula already gives the reference convention at r == 0
+  // for the smooth kernels (K(0) = valueAtZero); otherwise select explicitly.
+  const bool smooth = KID != FKTB_KERNEL_INVERSE_R && KID != FKTB_KERNEL_INVERSE_R2;
+  F.sel = !(smooth && A.kd.diag == F.wf);
+  if (F.sel)
+    near_fast<KID, D, true><<<tiles, kFastThreads, 0, st>>>(F);
+  else
+    near_fast<KID, D, false><<<tiles, kFastThreads, 0, st>>>(F);
+  FKTB_CUDA(cudaGetLastError());
+}
+
 template <int KID, int D>
 void launchNearT(const NearArgs& A, int tiles, cudaStream_t st) {
   const int d = D > 0 ? D : A.d;
@@ -112,6 +275,14 @@ void launchNearT(const NearArgs& A, int tiles, cudaStream_t st) {
 
 template <int KID>
 void launchNearK(const NearArgs& A, int tiles, cudaStream_t st) {
+  if constexpr (FastKernel<KID>::supported) {
+    switch (A.d) {
+      case 2: return launchFastT<KID, 2>(A, tiles, st);
+      case 3: return launchFastT<KID, 3>(A, tiles, st);
+      case 5: return launchFastT<KID, 5>(A, tiles, st);
+      default: break;
+    }
+  }
   switch (A.d) {
     case 2: return launchNearT<KID, 2>(A, tiles, st);
     case 3: return launchNearT<KID, 3>(A, tiles, st);
