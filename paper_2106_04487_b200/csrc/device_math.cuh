@@ -443,8 +443,9 @@ __device__ __forceinline__ void chain_degrees(const double* g, const double* cA,
 }
 
 template <int D, int P>
-__device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, double (&Y)[ChainTable<D, P>::H]) {
-  const double inv = r > 0.0 ? 1.0 / r : 0.0;
+__device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, double (&Y)[ChainTable<D, P>::H],
+                                              double rinv = -1.0) {
+  const double inv = rinv >= 0.0 ? rinv : (r > 0.0 ? 1.0 / r : 0.0);
   double v[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) v[a] = x[a] * inv;

@@ -230,19 +230,6 @@ __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant_
   }
 }
 
-// 2^(j/64), j < 64, correctly rounded (host long double).
-const double* expTableDevice() {
-  static double* dev = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    double host[kExpTable];
-    for (int j = 0; j < kExpTable; ++j) host[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / kExpTable));
-    FKTB_CUDA(cudaMalloc(&dev, sizeof(host)));
-    FKTB_CUDA(cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice));
-  });
-  return dev;
-}
-
 template <int KID, int D>
 void launchFastT(const NearArgs& A, int tiles, cudaStream_t st) {
   FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice()};
@@ -292,6 +279,19 @@ void launchNearK(const NearArgs& A, int tiles, cudaStream_t st) {
 }
 
 }  // namespace
+
+// 2^(j/64), j < 64, correctly rounded (host long double).
+const double* expTableDevice() {
+  static double* dev = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    double host[kExpTable];
+    for (int j = 0; j < kExpTable; ++j) host[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / kExpTable));
+    FKTB_CUDA(cudaMalloc(&dev, sizeof(host)));
+    FKTB_CUDA(cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice));
+  });
+  return dev;
+}
 
 int nearTileSize() { return kNearThreads * kNearTPT; }
 

@@ -143,6 +143,9 @@ void destroyPlan(DevicePlan* plan);
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
 
+// 2^(j/64), j < 64, in device memory (shared by the exp tables of every kernel).
+const double* expTableDevice();
+
 // Kernel launchers (near.cu, far.cu, dense.cu).
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void launchS2M(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
