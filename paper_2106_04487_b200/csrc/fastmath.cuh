@@ -16,6 +16,10 @@
 namespace fktb {
 
 constexpr int kExpTable = 64;
+// Shared-memory copy: entry j replicated for 16 bank pairs,
+// tab[j * kExpRep + c]; lane L reads column L % 16 so a warp's 64-bit lookups
+// never conflict (ncu showed 3.9-way conflicts with a single copy).
+constexpr int kExpRep = 16;
 // Added to every squared pair distance: keeps rsqrt finite at r == 0 and is
 // below one ulp of any squared distance >= 1e-284.
 constexpr double kQBias = 1e-300;
@@ -56,7 +60,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y0, e, y0);
 }
 
-// e^-u for u >= 0 (underflows to ~0 past u = 708). tab: 2^(j/64), j < 64.
+// e^-u for u >= 0 (underflows to ~0 past u = 708). tab: the lane's column of
+// the replicated 2^(j/64) table (tab[j * kExpRep] = 2^(j/64)).
+template <int REP = kExpRep>
 __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ tab) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   constexpr double kInvStep = 92.332482616893656;  // 64 / ln 2
@@ -74,7 +80,7 @@ __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ t
   p = fma(f, p, 0.5);
   p = fma(f, p, 1.0);
   p = fma(f, p, 1.0);
-  const double tj = tab[k & (kExpTable - 1)];
+  const double tj = tab[(k & (kExpTable - 1)) * REP];
   const int e = k >> 6;  // arithmetic shift: floor(k / 64)
   const double scaled = __hiloint2double(__double2hiint(tj) + (e << 20), __double2loint(tj));
   return scaled * p;
@@ -82,4 +88,14 @@ __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ t
 
 }  // namespace fktb
 
+#endif
+
+#ifndef FKTB_FASTMATH_FILL
+#define FKTB_FASTMATH_FILL
+namespace fktb {
+// Fill the replicated shared table from the 64-entry device table.
+__device__ __forceinline__ void fill_exp_table(double* tab, const double* src) {
+  for (int i = threadIdx.x; i < kExpTable * kExpRep; i += blockDim.x) tab[i] = src[i / kExpRep];
+}
+}  // namespace fktb
 #endif

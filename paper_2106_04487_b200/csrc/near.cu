@@ -19,7 +19,8 @@ namespace {
 
 constexpr int kNearThreads = 128;
 constexpr int kNearTPT = 2;
-constexpr int kNearChunk = 512;  // sources staged per pass
+constexpr int kNearChunk = 512;  // sources staged per pass (generic kernel)
+constexpr int kFastChunk = 512;  // sources staged per pass (fast kernel)
 
 struct NearArgs {
   int n, d, nrhs;
@@ -119,19 +120,20 @@ struct FastKernel {
       KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
       KID == FKTB_KERNEL_GAUSSIAN;
   // canonical K at scaled squared distance q (> 0 unless the select handles 0)
+  template <int REP>
   __device__ static __forceinline__ double eval(double q, const double* tab) {
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
       const double u = sqrt_nr(q);
-      const double e = exp_neg(u, tab);
+      const double e = exp_neg<REP>(u, tab);
       return fma(u, e, e);
     } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
-      return exp_neg(sqrt_nr(q), tab);
+      return exp_neg<REP>(sqrt_nr(q), tab);
     } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
       return rcp_nr(1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
       return rsqrt_nr(1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return exp_neg(q, tab);
+      return exp_neg<REP>(q, tab);
     } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
       return rsqrt_nr(q);
     } else {
@@ -164,7 +166,7 @@ struct FastArgs {
 template <int KID, int D, bool SEL>
 __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant__ FastArgs F) {
   constexpr int SP = (D + 2) / 2 * 2;  // AoS stride (coords + weight), even
-  __shared__ __align__(16) double ss[kNearChunk * SP];
+  __shared__ __align__(16) double ss[kFastChunk * SP];
   __shared__ double tab[kExpTable];
   const NearArgs& A = F.a;
   if constexpr (FastKernel<KID>::needsTable)
@@ -187,8 +189,8 @@ __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant_
   }
   for (int rhs = 0; rhs < A.nrhs; ++rhs) {
     const double* y = A.yp + static_cast<size_t>(rhs) * n;
-    for (int cs = sb; cs < se; cs += kNearChunk) {
-      const int cn = min(kNearChunk, se - cs);
+    for (int cs = sb; cs < se; cs += kFastChunk) {
+      const int cn = min(kFastChunk, se - cs);
       __syncthreads();
       for (int s = threadIdx.x; s < cn; s += kFastThreads) {
 #pragma unroll
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant_
             const double da = tx[i][a] - src[a];
             q = fma(da, da, q);
           }
-          double kv = FastKernel<KID>::eval(q, tab);
+          double kv = FastKernel<KID>::eval<1>(q, tab);
           if constexpr (SEL) kv = q == kQBias ? F.diagCanon : kv;
           acc[i] = fma(kv, w, acc[i]);
         }
