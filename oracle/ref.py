@@ -49,6 +49,11 @@ def lib():
             "fktref_dense_rows": (C.c_int, C.c_int, C.c_int, d, C.c_char_p, C.c_char_p, d, C.c_int,
                                   C.POINTER(C.c_int64), d, C.c_int, C.c_int, C.c_double),
             "fktref_fingerprints": (C.c_int, C.c_void_p, u64, u64, u64),
+            "fktref_tbar": (C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, d, C.c_char_p, C.c_int),
+            "fktref_compression_ranks": (C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_int, i32),
+            "fktref_addition_normalizer": (C.c_double, C.c_int, C.c_int),
+            "fktref_harmonics": (C.c_int, C.c_int, C.c_int, d, d),
+            "fktref_kernel_jet": (C.c_int, C.c_char_p, C.c_char_p, C.c_double, C.c_int, d),
         }
         for name, (res, *args) in sigs.items():
             f = getattr(L, name)
@@ -166,6 +171,42 @@ def dense_rows(x, kernel, params, y, rows, threads=0, diagonal=None):
                            float(diagonal or 0.0)) != 0:
         raise RuntimeError(L.fktref_last_error().decode())
     return z
+
+
+def tbar(d, p, k, j, m):
+    """(tbarDouble, 'num/den') from the reference's CoefficientTable."""
+    v = C.c_double()
+    buf = C.create_string_buffer(4096)
+    if lib().fktref_tbar(d, p, k, j, m, C.byref(v), buf, 4096) != 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return v.value, buf.value.decode()
+
+
+def compression_ranks(kernel, params, d, p):
+    ranks = (C.c_int * (p + 1))()
+    if lib().fktref_compression_ranks(kernel.encode(), _kv(params), d, p, ranks) != 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return list(ranks)
+
+
+def addition_normalizer(d, k):
+    return lib().fktref_addition_normalizer(d, k)
+
+
+def harmonics(d, p, point):
+    pt = np.ascontiguousarray(point, dtype=np.float64)
+    out = np.empty(4096)
+    cnt = lib().fktref_harmonics(d, p, _dp(pt), _dp(out))
+    if cnt < 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return out[:cnt]
+
+
+def kernel_jet(kernel, params, r, order):
+    out = np.empty(order + 1)
+    if lib().fktref_kernel_jet(kernel.encode(), _kv(params), r, order, _dp(out)) != 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return out
 
 
 def fingerprint_arrays(order, far_off, far, near_off, near, radius, center):

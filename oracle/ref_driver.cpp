@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "fkt/harmonics.hpp"
 #include "fkt/synthetic.hpp"
 #include "fkt/transform.hpp"
 
@@ -299,6 +300,66 @@ int fktref_dense_rows(int n, int d, const double* x, const char* kernel, const c
       });
     for (auto& t : pool) t.join();
     if (err) std::rethrow_exception(err);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Exact T-bar_kjm of the reference table (coefficients.cpp:102-106) as
+// "num/den", and its double (tbarDouble, :108-111).
+int fktref_tbar(int d, int p, int k, int j, int m, double* value, char* buf, int len) {
+  try {
+    const auto& t = fkt::coefficientTable(d, p);
+    const auto& q = t.tbar(k, j, m);
+    *value = t.tbarDouble(k, j, m);
+    std::ostringstream os;
+    os << numerator(q) << "/" << denominator(q);
+    std::snprintf(buf, static_cast<std::size_t>(len), "%s", os.str().c_str());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Compression ranks per degree (expansion.cpp:190-243).
+int fktref_compression_ranks(const char* kernel, const char* params, int d, int p, int* ranks) {
+  try {
+    auto k = fkt::makeKernel(kernel, parseParams(params));
+    auto f = fkt::radialCompression(*k, fkt::coefficientTable(d, p), p);
+    for (int i = 0; i <= p; ++i) ranks[i] = f[static_cast<std::size_t>(i)].rank;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Z_k (harmonics.cpp:114-116) and the orthonormal harmonic values at a point
+// (harmonics.cpp:160-246), degree-major.
+double fktref_addition_normalizer(int d, int k) { return fkt::additionNormalizer(d, k); }
+
+int fktref_harmonics(int d, int p, const double* point, double* values) {
+  try {
+    fkt::HarmonicBasis basis(d, p);
+    std::vector<double> v;
+    basis.evaluate(std::span<const double>(point, static_cast<std::size_t>(d)), v);
+    std::memcpy(values, v.data(), v.size() * sizeof(double));
+    return static_cast<int>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Kernel value and jet (kernels.hpp:49-64) for the builtin kernels.
+int fktref_kernel_jet(const char* kernel, const char* params, double r, int order, double* c) {
+  try {
+    auto k = fkt::makeKernel(kernel, parseParams(params));
+    const fkt::Jet j = k->jetAt(r, order);
+    for (int m = 0; m <= order; ++m) c[m] = j.coeff(m);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

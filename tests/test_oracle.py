@@ -1,0 +1,158 @@
+"""CPU: pin the oracle (exact tables + plain-C restatement) against the
+reference's own known-answer tests, the SURVEY Appendix A fingerprints, the
+golden fixtures generated from the reference, and (when built here) the
+reference library itself."""
+import json
+import math
+import os
+from fractions import Fraction as Q
+
+import numpy as np
+import pytest
+
+from oracle import restated as R
+from oracle import tables as T
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+# SURVEY Appendix A (reference tree.cpp on the Appendix B inputs).
+APPENDIX_A = {
+    1: ("03be6ceeb017b7b9", "230f744ce63833b3", "48e1f8bf59f104c1"),
+    2: ("8c7f8e136078a429", "c760e8fda6ec5e85", "416c6cce14efa277"),
+    3: ("104e01b90529b7d1", "ea7defe513db358c", "2f0f72757e65d118"),
+    4: ("dc858d5099c5d5fd", "40670ee71fa87916", "259560e62cca68f1"),
+    5: ("16ccdf33f0766b37", "ea5e9ae9d59d8e3d", "56eddb96a6f8255d"),
+}
+CFG = {1: (512, 0.5), 2: (512, 0.5), 3: (1024, 0.75), 4: (512, 0.5), 5: (512, 0.75)}
+
+
+# --- exact tables vs the reference's known-answer tests ------------------------
+def test_bell_kats():  # reference tests/test_coefficients.cpp:15-21
+    assert T.bell(1, 1) == Q(1, 2)
+    assert T.bell(3, 1) == Q(3, 8)
+    assert T.bell(2, 2) == Q(1, 4)
+    assert T.bell(2, 1) == Q(-1, 4)
+
+
+def test_tbar_kats():  # reference tests/test_coefficients.cpp:121-135
+    t = T.tbar_table(3, 8)
+    assert t[(1, 1, 1)] == -1
+    assert t[(0, 2, 1)] == Q(1, 3)
+    assert t[(0, 2, 2)] == Q(1, 6)
+    assert t[(0, 4, 1)] == 0 and t[(0, 4, 2)] == 0
+    assert t[(0, 4, 3)] == Q(1, 30)
+    assert t[(0, 4, 4)] == Q(1, 120)
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 9])
+def test_cosine_powers_reexpand(d):  # reference tests/test_coefficients.cpp:52-113
+    # sum_k A_ki C_k^(alpha)(x) == x^i, Gegenbauer polynomials built independently
+    maxi = 8
+    if d == 2:
+        tch = [[Q(1)], [Q(0), Q(1)]]
+        for k in range(2, maxi + 1):
+            cur = [Q(0)] * (k + 1)
+            for i, c in enumerate(tch[k - 1]):
+                cur[i + 1] += 2 * c
+            for i, c in enumerate(tch[k - 2]):
+                cur[i] -= c
+            tch.append(cur)
+        polys = [[Q(1)]] + [[Q(2, k) * c for c in tch[k]] for k in range(1, maxi + 1)]
+    else:
+        alpha = Q(d - 2, 2)
+        polys = [[Q(1)], [Q(0), 2 * alpha]]
+        for k in range(2, maxi + 1):
+            cur = [Q(0)] * (k + 1)
+            f1, f2 = 2 * (alpha + k - 1) / k, (k + 2 * alpha - 2) / k
+            for i, c in enumerate(polys[k - 1]):
+                cur[i + 1] += f1 * c
+            for i, c in enumerate(polys[k - 2]):
+                cur[i] -= f2 * c
+            polys.append(cur)
+    for i in range(maxi + 1):
+        a = T.cosine_power(d, i)
+        acc = [Q(0)] * (i + 1)
+        for k in range(i + 1):
+            for tt, c in enumerate(polys[k]):
+                acc[tt] += a[k] * c
+        assert acc == [Q(0)] * i + [Q(1)]
+
+
+def test_published_table3_ranks():  # reference tests/test_compression.cpp:121-151
+    rows = [("inverse-r", [1, 0, 2, 0, 3, 0, 4]), ("inverse-r2", [0, 1, 0, 2, 0, 3, 0]),
+            ("inverse-r3", [0, 0, 1, 0, 2, 0, 3]), ("exp-over-r", [1, 0, 2, 0, 3, 0, 4]),
+            ("exponential", [2, 0, 3, 0, 4, 0, 5]), ("r-exp", [3, 0, 4, 0, 5, 0, 6])]
+    p = 12
+    for name, ra in rows:
+        for d in range(3, 10):
+            f = T.radial_compression(name, {}, d, p)
+            for k in range(p + 1):
+                bound = (p - k + 2) // 2
+                want = bound if ra[d - 3] == 0 else min(ra[d - 3], bound)
+                assert f[k][0] == want, (name, d, k)
+
+
+def test_harmonic_normalizers():  # reference tests/test_harmonics.cpp:136-151
+    for k in range(8):
+        assert math.isclose(T.addition_normalizer(3, k), 4 * math.pi / (2 * k + 1), rel_tol=1e-14)
+    assert math.isclose(T.addition_normalizer(4, 1), math.pi ** 2, rel_tol=1e-14)
+    for d in range(2, 7):
+        for k in range(6):
+            assert len(T.chains(d, k)) == T.harmonic_count(d, k)
+
+
+# --- the restated tree / sets against SURVEY Appendix A ---------------------------
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_restated_tree_fingerprints(fkt, cfg):
+    n = {1: 20000, 2: 1000000, 3: 1000000, 4: 4000000, 5: 2000000}[cfg]
+    x, _ = fkt.synthConfig(cfg, n)  # product generator (bit-identical to fkt::Rng, test_cabi.py)
+    leaf, theta = CFG[cfg]
+    t = R.RestatedTree(x, leaf).sets(theta)
+    assert t.fingerprints() == APPENDIX_A[cfg]
+
+
+def test_restated_z_matches_reference_golden(fkt):
+    g = np.load(os.path.join(GOLDEN, "cfg1_ref.npz"))
+    x, w = fkt.synthConfig(1, 20000)
+    t = R.RestatedTree(x, 512).sets(0.5)
+    z = t.multiply("cauchy", {"sigma": 1.0}, 4, w)
+    assert np.linalg.norm(z - g["z"]) / np.linalg.norm(g["z"]) <= 1e-12
+    meta = json.load(open(os.path.join(GOLDEN, "cfg1_ref.json")))
+    assert (meta["order"], meta["sets"], meta["geom"]) == APPENDIX_A[1]
+
+
+def test_restated_dense_rows_match_golden(fkt):
+    g = np.load(os.path.join(GOLDEN, "cfg1_ref.npz"))
+    x, w = fkt.synthConfig(1, 20000)
+    zd = R.dense_rows(x, "cauchy", {"sigma": 1.0}, w, g["rows"][:200])
+    assert np.linalg.norm(zd - g["dense_rows"][:200]) / np.linalg.norm(g["dense_rows"][:200]) <= 1e-14
+
+
+# --- restatement vs the reference library itself (when built here) ----------------
+CASES = [("gaussian", {}, 3, 1), ("gaussian", {}, 3, 2), ("inverse-r", {}, 3, 0),
+         ("matern32", {"sigma": 0.9, "rho": 0.4}, 2, 0), ("exp-neg-inv-r2", {}, 4, 0), ("cos-over-r", {}, 5, 0),
+         ("rational-quadratic", {"sigma": 1.3}, 3, 0), ("matern12", {"sigma": 2.0, "rho": 0.3}, 3, 1)]
+
+
+@pytest.mark.parametrize("name,params,d,comp", CASES)
+def test_restated_matches_reference(ref, name, params, d, comp):
+    x, y = ref.gen_cloud("mixture", 1500, d, 3)
+    rp = ref.RefPlan(x, name, params, p=5, theta=0.6, leaf=64, compression=comp)
+    t = R.RestatedTree(x, 64).sets(0.6)
+    assert t.fingerprints() == rp.fingerprints()
+    z, zr = t.multiply(name, params, 5, y, compression=comp), rp.multiply(y)
+    assert np.linalg.norm(z - zr) / np.linalg.norm(zr) <= 1e-13
+
+
+def test_tables_match_reference(ref):
+    for d, p in [(2, 6), (3, 8), (5, 4), (4, 6)]:
+        tt = T.tbar_table(d, p)
+        for (k, j, m), q in list(tt.items())[::3]:
+            v, s = ref.tbar(d, p, k, j, m)
+            assert Q(s) == q and v == float(q)
+    for name in ["gaussian", "inverse-r", "exponential", "exp-neg-inv-r"]:
+        for d, p in [(3, 8), (5, 4), (2, 6)]:
+            assert [r for r, _, _ in T.radial_compression(name, {}, d, p)] == ref.compression_ranks(name, {}, d, p)
+    for d in range(2, 7):
+        for k in range(7):
+            assert T.addition_normalizer(d, k) == pytest.approx(ref.addition_normalizer(d, k), rel=1e-15)
