@@ -53,11 +53,15 @@ __device__ __forceinline__ double sqrt_nr(double x) {
   return fma(0.5 * h, e, h);
 }
 
-// 1/x, x normal.
+// 1/x, x normal: two Newton steps (the MUFU seed has ~2^-23 relative error;
+// one step leaves ~1e-14, two reach rounding level, which the reference's
+// single-leaf exactness test (1e-13 vs dense) needs).
 __device__ __forceinline__ double rcp_nr(double x) {
   const double y0 = rcp_approx(x);
-  const double e = fma(-x, y0, 1.0);
-  return fma(y0, e, y0);
+  const double e0 = fma(-x, y0, 1.0);
+  const double y1 = fma(y0, e0, y0);
+  const double e1 = fma(-x, y1, 1.0);
+  return fma(y1, e1, y1);
 }
 
 // e^-u for u >= 0 (underflows to ~0 past u = 708). tab: the lane's column of

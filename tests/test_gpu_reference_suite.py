@@ -1,0 +1,280 @@
+"""The reference's own test strategy (proj/tests/test_tree.cpp,
+test_transform.cpp) ported to the GPU implementation, plus edge cases
+(duplicates, zero extent, tiny clouds, degenerate geometry, diagonal
+conventions) compared bit-for-bit / to 1e-10 against the reference."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def P(fkt, x):
+    return fkt.PointCloud.from_array(np.asarray(x, dtype=np.float64))
+
+
+def tree_matches_reference(fkt, ref, x, leaf, theta):
+    t = fkt.PartitionTree(P(fkt, x), leaf)
+    t.computeInteractionSets(theta)
+    rp = ref.RefPlan(x, "cauchy", {}, p=1, theta=theta, leaf=leaf)
+    rt = rp.tree()
+    np.testing.assert_array_equal(t.order(), rt["order"])
+    np.testing.assert_array_equal(t.begins, rt["begin"])
+    np.testing.assert_array_equal(t.lefts, rt["left"])
+    np.testing.assert_array_equal(t.radii.view(np.uint64), rt["radius"].view(np.uint64))
+    np.testing.assert_array_equal(t.centers.view(np.uint64), rt["center"].view(np.uint64))
+    fo, fi = t.farCsr()
+    no, ni = t.nearCsr()
+    np.testing.assert_array_equal(fo, rt["farOff"])
+    np.testing.assert_array_equal(fi, rt["far"])
+    np.testing.assert_array_equal(no, rt["nearOff"])
+    np.testing.assert_array_equal(ni, rt["near"])
+    return t
+
+
+# --- test_tree.cpp ---------------------------------------------------------------
+def test_tree_structure_invariants(fkt):  # test_tree.cpp:14-48
+    x, _ = fkt.synthCloud("cube", 5000, 3, 5)
+    t = fkt.PartitionTree(P(fkt, x), 64)
+    for b in range(t.nodeCount()):
+        nd = t.node(b)
+        side = nd.boxHi - nd.boxLo
+        assert side.max() <= 2.0 * side.min() + 1e-12
+        if nd.isLeaf():
+            assert nd.count() <= 64
+        else:
+            assert t.node(nd.left).begin == nd.begin and t.node(nd.right).end == nd.end
+            assert t.node(nd.left).end == t.node(nd.right).begin
+        pts = t.points()[nd.begin:nd.end]
+        assert np.sqrt(((pts - nd.center) ** 2).sum(1)).max() <= nd.radius * (1 + 1e-15)
+
+
+def test_exact_coverage(fkt):  # test_tree.cpp:51-79
+    x, _ = fkt.synthCloud("sphere", 3000, 3, 9)
+    t = fkt.PartitionTree(P(fkt, x), 100)
+    t.computeInteractionSets(0.6)
+    fo, fi = t.farCsr()
+    no, ni = t.nearCsr()
+    for b in range(t.nodeCount()):
+        nd = t.node(b)
+        if not nd.isLeaf():
+            continue
+        # ancestors of this leaf
+        path, cur = [], 0
+        while True:
+            path.append(cur)
+            c = t.node(cur)
+            if c.isLeaf():
+                break
+            cur = c.left if t.node(c.left).begin <= nd.begin < t.node(c.left).end else c.right
+        cover = np.zeros(3000, int)
+        for a in path:
+            cover[fi[fo[a]:fo[a + 1]]] += 1
+        cover[ni[no[b]:no[b + 1]]] += 1
+        assert (cover == 1).all()
+
+
+def test_far_criterion(fkt):  # test_tree.cpp:81-94
+    x, _ = fkt.synthCloud("cube", 4000, 2, 3)
+    t = fkt.PartitionTree(P(fkt, x), 50)
+    t.computeInteractionSets(0.5)
+    fo, fi = t.farCsr()
+    for b in range(t.nodeCount()):
+        nd = t.node(b)
+        far = x[fi[fo[b]:fo[b + 1]]]
+        if len(far):
+            assert (np.sqrt(((far - nd.center) ** 2).sum(1)) > nd.radius / 0.5).all()
+
+
+def test_two_cluster_far_claim(fkt, ref):  # test_tree.cpp:149-171
+    rng = np.random.default_rng(4)
+    x = np.vstack([rng.random((300, 3)) * 0.1, rng.random((300, 3)) * 0.1 + 10.0])
+    tree_matches_reference(fkt, ref, x, 64, 0.5)
+
+
+@pytest.mark.parametrize("n,leaf", [(1, 512), (2, 1), (7, 1), (513, 512), (1000, 1), (2000, 3)])
+def test_small_and_leaf_capacity_edges(fkt, ref, n, leaf):
+    x, _ = fkt.synthCloud("cube", n, 3, 21)
+    tree_matches_reference(fkt, ref, x, leaf, 0.5)
+
+
+def test_duplicates_and_zero_extent(fkt, ref):  # test_tree.cpp:173-199
+    x = np.tile(np.array([[0.25, 0.5, 0.75]]), (900, 1))  # all identical: zero-extent root leaf
+    t = tree_matches_reference(fkt, ref, x, 16, 0.5)
+    assert t.nodeCount() == 1
+    rng = np.random.default_rng(5)
+    base = rng.random((40, 3))
+    x2 = np.repeat(base, 25, axis=0)  # 25 duplicates of each of 40 points
+    tree_matches_reference(fkt, ref, x2, 8, 0.5)
+
+
+def test_degenerate_geometry(fkt, ref):
+    rng = np.random.default_rng(6)
+    line = np.zeros((3000, 3))
+    line[:, 0] = rng.random(3000)  # collinear: regularisation pads the short sides
+    tree_matches_reference(fkt, ref, line, 32, 0.5)
+    plane = np.zeros((3000, 4))
+    plane[:, :2] = rng.random((3000, 2))
+    tree_matches_reference(fkt, ref, plane, 32, 0.7)
+    grid = np.stack(np.meshgrid(np.arange(20.0), np.arange(20.0), np.arange(5.0)), -1).reshape(-1, 3)
+    tree_matches_reference(fkt, ref, grid, 16, 0.5)  # many ties at the median
+
+
+def test_theta_validation(fkt):
+    t = fkt.PartitionTree(P(fkt, np.random.default_rng(1).random((100, 2))), 16)
+    for bad in (0.0, 1.0, -0.5, 1.5):
+        with pytest.raises(fkt.InvalidArgument):
+            t.computeInteractionSets(bad)
+
+
+def test_determinism(fkt):  # test_tree.cpp:201-216
+    x, _ = fkt.synthCloud("mixture", 20000, 3, 8)
+    a = fkt.PartitionTree(P(fkt, x), 128)
+    a.computeInteractionSets(0.5)
+    b = fkt.PartitionTree(P(fkt, x), 128)
+    b.computeInteractionSets(0.5)
+    np.testing.assert_array_equal(a.order(), b.order())
+    np.testing.assert_array_equal(a.farCsr()[1], b.farCsr()[1])
+
+
+# --- test_transform.cpp -------------------------------------------------------------
+def test_single_leaf_exact(fkt):  # :38-50
+    x, y = fkt.synthCloud("cube", 300, 3, 42)
+    k = fkt.makeKernel("cauchy")
+    p = fkt.plan(P(fkt, x), k, fkt.FktOptions(leafCapacity=512))
+    assert p.tree().nodeCount() == 1
+    assert fkt.relativeError(p.multiply(y), fkt.denseMultiply(P(fkt, x), k, y)) < 1e-13
+
+
+def test_oracle_equivalence(fkt, ref):  # :78-99
+    # The reference's absolute bound (1e-3) is not met by the reference itself
+    # (oracle/ref_selfcheck.cpp); the contract is equality with the reference
+    # FKT, whose dense error we reproduce.
+    for d in (2, 3, 4, 5):
+        for name in ("exponential", "cauchy", "gaussian", "matern32"):
+            x, y = fkt.synthCloud("sphere" if d % 2 else "cube", 1500, d, 100 + d)
+            k = fkt.makeKernel(name)
+            p = fkt.plan(P(fkt, x), k, fkt.FktOptions(p=4, theta=0.75, leafCapacity=128))
+            z = p.multiply(y)
+            zd = fkt.denseMultiply(P(fkt, x), k, y)
+            rp = ref.RefPlan(x, name, {}, p=4, theta=0.75, leaf=128)
+            zr = rp.multiply(y)
+            assert fkt.relativeError(z, zr) <= 1e-10
+            assert fkt.relativeError(z, zd) == pytest.approx(fkt.relativeError(zr, zd), rel=1e-6)
+            assert fkt.relativeError(z, zd) < 5e-2
+
+
+def test_error_decreases_with_p(fkt, ref):  # :101-118
+    x, y = fkt.synthCloud("sphere", 1200, 3, 88)
+    k = fkt.makeKernel("exponential")
+    exact = fkt.denseMultiply(P(fkt, x), k, y)
+    prev = 1e9
+    for p in (2, 4, 6, 8):
+        z = fkt.plan(P(fkt, x), k, fkt.FktOptions(p=p, leafCapacity=128)).multiply(y)
+        err = fkt.relativeError(z, exact)
+        assert err < prev * 2.0
+        assert fkt.relativeError(z, ref.RefPlan(x, "exponential", {}, p=p, leaf=128).multiply(y)) <= 1e-10
+        prev = err
+    assert prev < 1e-3  # reference asserts 1e-6; it reaches 2.8e-4 itself (oracle/ref_selfcheck.cpp)
+
+
+def test_symmetry_probe(fkt):  # :166-186
+    x, _ = fkt.synthCloud("cube", 700, 3, 606)
+    k = fkt.makeKernel("exponential")
+    p = fkt.plan(P(fkt, x), k, fkt.FktOptions(leafCapacity=64))
+    yref = np.random.default_rng(1).standard_normal(700)
+    dense_err = fkt.relativeError(p.multiply(yref), fkt.denseMultiply(P(fkt, x), k, yref)) + 1e-300
+    ei, ej = np.zeros(700), np.zeros(700)
+    ei[13] = ej[521] = 1.0
+    zi = p.multiply(ei)
+    assert abs(zi[521] - p.multiply(ej)[13]) <= 10 * dense_err * np.linalg.norm(zi) + 1e-12
+
+
+def test_node_count_bound(fkt):  # :233-241
+    x, _ = fkt.synthCloud("sphere", 10000, 3, 3121)
+    p = fkt.plan(P(fkt, x), fkt.makeKernel("matern12"))
+    ideal = 2 * math.ceil(10000 / 512) - 1
+    assert ideal <= p.tree().nodeCount() <= 4 * ideal
+
+
+def test_plan_errors(fkt):
+    x, y = fkt.synthCloud("cube", 100, 2, 1)
+    k = fkt.makeKernel("exponential")
+    p = fkt.plan(P(fkt, x), k)
+    with pytest.raises(fkt.DimensionMismatchError):
+        p.multiply(np.zeros(99))
+    with pytest.raises(fkt.OrderTooLargeError):
+        fkt.plan(P(fkt, x), k, fkt.FktOptions(p=21))
+    with pytest.raises(fkt.InvalidArgument):
+        fkt.plan(P(fkt, x), k, fkt.FktOptions(p=-1))
+    with pytest.raises(fkt.InvalidArgument):
+        fkt.plan(P(fkt, x), k, fkt.FktOptions(theta=1.0))
+    with pytest.raises(fkt.InvalidArgument):
+        fkt.plan(P(fkt, x), k, fkt.FktOptions(leafCapacity=0))
+    with pytest.raises(fkt.NotRecurrenceKernelError):
+        fkt.plan(P(fkt, x), fkt.makeKernel("matern32"), fkt.FktOptions(compression=fkt.CompressionMode.On))
+    with pytest.raises(fkt.UnsupportedOnGpuError):
+        fkt.plan(P(fkt, x), k, fkt.FktOptions(barnesHut=True))
+    with pytest.raises(fkt.DimensionMismatchError):
+        fkt.denseMultiply(P(fkt, x), k, np.zeros(3))
+
+
+# --- conventions and RHS variants vs the reference ------------------------------------
+@pytest.mark.parametrize("name,diag", [("inverse-r", None), ("inverse-r", 2.5), ("cauchy", 7.0),
+                                       ("matern32", None), ("gaussian", 0.0)])
+def test_diagonal_conventions_with_duplicates(fkt, ref, name, diag):
+    rng = np.random.default_rng(12)
+    x = np.repeat(rng.random((600, 3)), 3, axis=0)  # every point three times
+    y = rng.standard_normal(1800)
+    prm = {"sigma": 1.0, "rho": 0.3} if name == "matern32" else {}
+    p = fkt.plan(P(fkt, x), fkt.makeKernel(name, prm), fkt.FktOptions(p=4, theta=0.6, leafCapacity=64,
+                                                                     diagonal=diag))
+    rp = ref.RefPlan(x, name, prm, p=4, theta=0.6, leaf=64, diagonal=diag)
+    assert fkt.relativeError(p.multiply(y), rp.multiply(y)) <= 1e-10
+    zd = fkt.denseMultiply(P(fkt, x), fkt.makeKernel(name, prm), y, diagonal=diag)
+    assert fkt.relativeError(zd, ref.dense(x, name, prm, y, diagonal=diag)) <= 1e-12
+
+
+def test_multi_rhs_equals_columns(fkt, ref):
+    x, W = fkt.synthConfig(5, 30000)
+    p = fkt.plan(P(fkt, x), fkt.makeKernel("cauchy", {"sigma": 1.0}), fkt.FktOptions(p=6, leafCapacity=512))
+    Z = p.multiply(W)
+    rp = ref.RefPlan(x, "cauchy", {"sigma": 1.0}, p=6, theta=0.75, leaf=512)
+    Zr = rp.multiply(W)
+    for r in range(W.shape[1]):
+        assert fkt.relativeError(Z[:, r], Zr[:, r]) <= 1e-10
+        assert fkt.relativeError(Z[:, r], p.multiply(np.ascontiguousarray(W[:, r]))) <= 1e-13
+
+
+def test_device_multiply_matches_host(fkt):
+    import torch
+
+    x, w = fkt.synthConfig(2, 50000)
+    p = fkt.plan(P(fkt, x), fkt.makeKernel("matern32", {"sigma": 1.0, "rho": 0.1}),
+                 fkt.FktOptions(p=6, theta=0.5, leafCapacity=512))
+    zh = p.multiply(w)
+    zd = p.multiply_device(torch.from_numpy(w).cuda()).cpu().numpy()
+    assert fkt.relativeError(zd, zh) <= 1e-14
+
+
+@pytest.mark.parametrize("d", [1, 6, 7])
+def test_unusual_dimensions(fkt, ref, d):
+    x, y = fkt.synthCloud("cube", 2000, d, 33)
+    if d == 1:  # the tree exists for d = 1; the harmonic basis needs d >= 2 (harmonics.cpp:119)
+        from oracle import restated as R
+
+        t = fkt.PartitionTree(P(fkt, x), 32)
+        t.computeInteractionSets(0.5)
+        rt = R.RestatedTree(x, 32).sets(0.5)  # the C restatement (pinned to the reference)
+        np.testing.assert_array_equal(t.order(), rt.order)
+        np.testing.assert_array_equal(t.centers.view(np.uint64), rt.center.view(np.uint64))
+        np.testing.assert_array_equal(t.farCsr()[1], rt.far)
+        np.testing.assert_array_equal(t.nearCsr()[1], rt.near)
+        with pytest.raises(fkt.InvalidArgument):
+            fkt.plan(P(fkt, x), fkt.makeKernel("gaussian"))
+        return
+    p = fkt.plan(P(fkt, x), fkt.makeKernel("gaussian"), fkt.FktOptions(p=3, theta=0.7, leafCapacity=64))
+    rp = ref.RefPlan(x, "gaussian", {}, p=3, theta=0.7, leaf=64)
+    assert p.coefficientCount() == rp.coef
+    assert fkt.relativeError(p.multiply(y), rp.multiply(y)) <= 1e-10
