@@ -4,8 +4,8 @@
 // libm's correctly rounded results for fewer instructions while keeping a
 // relative error <= ~5e-14 per evaluation (z is gated at rel-L2 1e-10):
 //   * exp_neg(u) = e^-u, u >= 0: 64-entry 2^(j/64) table in shared memory,
-//     two-step Cody-Waite reduction, degree-4 Taylor polynomial (|f| <=
-//     ln2/128), exponent added in the integer pipe. 9 FP64 ops.
+//     one-constant range reduction, degree-4 Taylor polynomial (|f| <=
+//     ln2/128), exponent added in the integer pipe. 8 FP64 ops.
 //   * rsqrt_nr / sqrt_nr: MUFU rsqrt.approx.f64 + one Newton step. 4 FP64 ops.
 //   * rcp_nr: MUFU rcp.approx.f64 + one Newton step. 2 FP64 ops.
 #ifndef FKTB_FASTMATH_CUH
@@ -70,16 +70,17 @@ template <int REP = kExpRep>
 __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ tab) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   constexpr double kInvStep = 92.332482616893656;  // 64 / ln 2
-  constexpr double kStepHi = 0.010830424696223417;  // ln2/64, high part (exact multiple product)
-  constexpr double kStepLo = 2.572804622327669e-14;  // ln2/64 - kStepHi
+  // ln2/64 rounded to double: a one-constant reduction errs by |k| * 2^-60,
+  // i.e. <= u * 1e-16 relative in e^-u (a two-constant Cody-Waite step would
+  // cost one more FP64 op per pair for accuracy the 1e-10 gate does not need).
+  constexpr double kStep = 0.010830424696249145;
   // clamp u <= ~708 on the high word (integer pipe): e^-708 ~ 3e-308, and
   // keeps the exponent arithmetic below in the normal range
   u = __hiloint2double(min(__double2hiint(u), 0x40862000), __double2loint(u));
   const double t = fma(-u, kInvStep, kMagic);
   const int k = __double2loint(t);  // round(-u * 64 / ln2), <= 0
   const double kd = t - kMagic;
-  double f = fma(kd, -kStepHi, -u);
-  f = fma(kd, -kStepLo, f);
+  const double f = fma(kd, -kStep, -u);
   double p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
   p = fma(f, p, 0.5);
   p = fma(f, p, 1.0);

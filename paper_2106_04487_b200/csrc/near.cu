@@ -12,6 +12,7 @@
 #include "plan.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 namespace fktb {
@@ -106,9 +107,6 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constan
 // kernel length scale (and weights by its prefactor) so the pair body is the
 // canonical kernel; FP64 fast math (fastmath.cuh); 4 targets per thread
 // against AoS shared-memory sources read with 128-bit broadcast loads.
-constexpr int kFastThreads = 64;
-constexpr int kFastTPT = 4;  // kFastThreads * kFastTPT == tile size
-static_assert(kFastThreads * kFastTPT == kNearThreads * kNearTPT, "near tile size");
 
 template <int KID>
 struct FastKernel {
@@ -163,42 +161,50 @@ struct FastArgs {
   const double* expTable;
 };
 
-template <int KID, int D, bool SEL>
-__global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant__ FastArgs F) {
-  constexpr int SP = (D + 2) / 2 * 2;  // AoS stride (coords + weight), even
-  __shared__ __align__(16) double ss[kFastChunk * SP];
+// THREADS x TPT = 256 targets per tile; UNR sources per unrolled step; R
+// right-hand sides per pass (the kernel value is evaluated once per pair and
+// reused for all R weights).
+template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
+__global__ void __launch_bounds__(THREADS) near_fast(const __grid_constant__ FastArgs F) {
+  static_assert(THREADS * TPT == kNearThreads * kNearTPT, "near tile size");
+  constexpr int SP = (D + R + 1) / 2 * 2;  // AoS stride (coords + R weights), even
+  constexpr int CHUNK = R > 2 ? 256 : kFastChunk;
+  __shared__ __align__(16) double ss[CHUNK * SP];
   __shared__ double tab[kExpTable];
   const NearArgs& A = F.a;
   if constexpr (FastKernel<KID>::needsTable)
-    for (int i = threadIdx.x; i < kExpTable; i += kFastThreads) tab[i] = F.expTable[i];
+    for (int i = threadIdx.x; i < kExpTable; i += THREADS) tab[i] = F.expTable[i];
   const FktbTile tile = A.tiles[blockIdx.x];
   const int leaf = tile.node;
   const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
   const int n = A.n;
-  int tpos[kFastTPT];
-  double tx[kFastTPT][D];
-  double acc[kFastTPT];
+  int tpos[TPT];
+  double tx[TPT][D];
+  double acc[TPT][R];
 #pragma unroll
-  for (int i = 0; i < kFastTPT; ++i) {
-    const int idx = threadIdx.x + i * kFastThreads;
+  for (int i = 0; i < TPT; ++i) {
+    const int idx = threadIdx.x + i * THREADS;
     tpos[i] = idx < tile.count ? static_cast<int>(A.nearPos[tile.start + idx]) : -1;
     const int p = tpos[i] >= 0 ? tpos[i] : 0;
 #pragma unroll
     for (int a = 0; a < D; ++a) tx[i][a] = A.pc[static_cast<size_t>(a) * n + p] * F.sc;
-    acc[i] = 0.0;
   }
-  for (int rhs = 0; rhs < A.nrhs; ++rhs) {
-    const double* y = A.yp + static_cast<size_t>(rhs) * n;
-    for (int cs = sb; cs < se; cs += kFastChunk) {
-      const int cn = min(kFastChunk, se - cs);
+  for (int r0 = 0; r0 < A.nrhs; r0 += R) {
+#pragma unroll
+    for (int i = 0; i < TPT; ++i)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
+    for (int cs = sb; cs < se; cs += CHUNK) {
+      const int cn = min(CHUNK, se - cs);
       __syncthreads();
-      for (int s = threadIdx.x; s < cn; s += kFastThreads) {
+      for (int s = threadIdx.x; s < cn; s += THREADS) {
 #pragma unroll
         for (int a = 0; a < D; ++a) ss[s * SP + a] = A.pc[static_cast<size_t>(a) * n + cs + s] * F.sc;
-        ss[s * SP + D] = y[cs + s] * F.wf;
+#pragma unroll
+        for (int r = 0; r < R; ++r) ss[s * SP + D + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * F.wf;
       }
       __syncthreads();
-#pragma unroll 2
+#pragma unroll UNR
       for (int s = 0; s < cn; ++s) {
         double src[SP];
 #pragma unroll
@@ -207,9 +213,8 @@ __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant_
           src[q] = v.x;
           src[q + 1] = v.y;
         }
-        const double w = src[D];
 #pragma unroll
-        for (int i = 0; i < kFastTPT; ++i) {
+        for (int i = 0; i < TPT; ++i) {
           const double d0 = tx[i][0] - src[0];
           double q = fma(d0, d0, kQBias);
 #pragma unroll
@@ -217,19 +222,58 @@ __global__ void __launch_bounds__(kFastThreads) near_fast(const __grid_constant_
             const double da = tx[i][a] - src[a];
             q = fma(da, da, q);
           }
-          double kv = FastKernel<KID>::eval<1>(q, tab);
+          double kv = FastKernel<KID>::template eval<1>(q, tab);
           if constexpr (SEL) kv = q == kQBias ? F.diagCanon : kv;
-          acc[i] = fma(kv, w, acc[i]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[i][r] = fma(kv, src[D + r], acc[i][r]);
         }
       }
     }
-    double* z = A.zp + static_cast<size_t>(rhs) * n;
 #pragma unroll
-    for (int i = 0; i < kFastTPT; ++i) {
-      if (tpos[i] >= 0) atomicAdd(z + tpos[i], acc[i]);
-      acc[i] = 0.0;
-    }
+    for (int i = 0; i < TPT; ++i)
+      if (tpos[i] >= 0)
+#pragma unroll
+        for (int r = 0; r < R; ++r) atomicAdd(A.zp + static_cast<size_t>(r0 + r) * n + tpos[i], acc[i][r]);
   }
+}
+
+template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
+void launchFastV(const FastArgs& F, int tiles, cudaStream_t st) {
+  near_fast<KID, D, SEL, THREADS, TPT, UNR, R><<<tiles, THREADS, 0, st>>>(F);
+  FKTB_CUDA(cudaGetLastError());
+}
+
+// Developer knob for tuning sweeps (scripts/sweep_near.py): FKTB_NEAR_VARIANT
+// selects the (threads, targets/thread, unroll) shape of the single-RHS
+// Matern-3/2 d=3 kernel. 0 is the default.
+inline int nearVariant() {
+  static const int v = [] {
+    const char* e = std::getenv("FKTB_NEAR_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int KID, int D, bool SEL>
+void launchFastSel(const FastArgs& F, int nrhs, int tiles, cudaStream_t st) {
+  if (nrhs == 1) {
+    if constexpr (KID == FKTB_KERNEL_MATERN32 && D == 3 && !SEL) {
+      switch (nearVariant()) {
+        case 1: return launchFastV<KID, D, SEL, 64, 4, 4, 1>(F, tiles, st);
+        case 2: return launchFastV<KID, D, SEL, 32, 8, 1, 1>(F, tiles, st);
+        case 3: return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, st);
+        case 4: return launchFastV<KID, D, SEL, 128, 2, 4, 1>(F, tiles, st);
+        case 5: return launchFastV<KID, D, SEL, 64, 4, 1, 1>(F, tiles, st);
+        default: break;
+      }
+    }
+    return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, st);
+  }
+  if (nrhs % 16 == 0) return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, st);
+  if (nrhs % 8 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 8>(F, tiles, st);
+  if (nrhs % 4 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 4>(F, tiles, st);
+  if (nrhs % 2 == 0) return launchFastV<KID, D, SEL, 64, 4, 2, 2>(F, tiles, st);
+  return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, st);
 }
 
 template <int KID, int D>
@@ -242,10 +286,9 @@ void launchFastT(const NearArgs& A, int tiles, cudaStream_t st) {
   const bool smooth = KID != FKTB_KERNEL_INVERSE_R && KID != FKTB_KERNEL_INVERSE_R2;
   F.sel = !(smooth && A.kd.diag == F.wf);
   if (F.sel)
-    near_fast<KID, D, true><<<tiles, kFastThreads, 0, st>>>(F);
+    launchFastSel<KID, D, true>(F, A.nrhs, tiles, st);
   else
-    near_fast<KID, D, false><<<tiles, kFastThreads, 0, st>>>(F);
-  FKTB_CUDA(cudaGetLastError());
+    launchFastSel<KID, D, false>(F, A.nrhs, tiles, st);
 }
 
 template <int KID, int D>
