@@ -170,7 +170,7 @@ def run_ours(args):
     x, w = fkt.synthConfig(args.cfg, n)
     t0 = time.perf_counter()
     pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(c["kernel"], c["params"]),
-                  fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"]))
+                  fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"], nearPrecision=args.near_precision))
     plan_s = time.perf_counter() - t0
     info = pl.info()
     wcols = w.reshape(n, nrhs) if nrhs > 1 else w
@@ -270,7 +270,7 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f64" if args.near_precision == 64 else "f64 (near field f32 fast mode)",
         "data": "synthetic (SURVEY Appendix B recipe, fkt::Rng(42); no public dataset)",
         "config": {
             "workload": workload_desc(args.cfg),
@@ -402,6 +402,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--near-precision", type=int, default=64, choices=[64, 32],
+                    help="32 = FP32 fast near-field mode (not the headline; parity gate is FP64)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -50,6 +50,7 @@ struct FktOptions {
   bool barnesHut = false;      // not offered on the GPU path
   int threads = 0;             // CPU knob of the reference, ignored
   std::optional<double> diagonal;
+  int nearPrecision = 64;      // additive: 32 selects the FP32 fast near field
 };
 
 class FktPlan {

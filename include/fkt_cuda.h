@@ -47,6 +47,7 @@ typedef struct fkt_options {
   int threads;         /* CPU-only knob, ignored */
   int has_diagonal;
   double diagonal;
+  int near_precision;  /* additive extension: 64 (default, FP64) or 32 (FP32 fast near field) */
 } fkt_options;
 
 typedef struct fkt_plan_s* fkt_plan_t;

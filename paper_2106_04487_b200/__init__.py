@@ -196,11 +196,12 @@ class FktOptions:
     barnesHut: bool = False
     threads: int = 0
     diagonal: Optional[float] = None
+    nearPrecision: int = 64  # additive: 32 selects the FP32 fast near field
 
     def _c(self) -> _L.FktOptionsC:
         return _L.FktOptionsC(int(self.p), float(self.theta), int(self.leafCapacity), int(self.compression),
                               int(bool(self.eagerOperators)), int(bool(self.barnesHut)), int(self.threads),
-                              int(self.diagonal is not None), float(self.diagonal or 0.0))
+                              int(self.diagonal is not None), float(self.diagonal or 0.0), int(self.nearPrecision))
 
 
 # --- tree view -----------------------------------------------------------------

@@ -38,6 +38,7 @@ class FktOptionsC(C.Structure):
         ("threads", C.c_int),
         ("has_diagonal", C.c_int),
         ("diagonal", C.c_double),
+        ("near_precision", C.c_int),
     ]
 
 

@@ -240,6 +240,7 @@ FktPlan::FktPlan(PointCloud cloud, KernelPtr kernel, const FktOptions& options)
   o.threads = options_.threads;
   o.has_diagonal = options_.diagonal ? 1 : 0;
   o.diagonal = options_.diagonal.value_or(0.0);
+  o.near_precision = options_.nearPrecision;
   ParamArrays pa(kernel_->parameters());
   fkt_plan_t h = nullptr;
   check(fkt_plan_create(cloud_.n, cloud_.d, cloud_.x.data(), kernel_->name().c_str(), pa.k(), pa.v(), pa.n(), &o, &h));

@@ -156,6 +156,7 @@ void fkt_default_options(fkt_options* o) {
   o->threads = 0;
   o->has_diagonal = 0;
   o->diagonal = 0.0;
+  o->near_precision = 64;
 }
 
 int fkt_plan_create(int n, int d, const double* x, const char* kernel, const char* const* keys, const double* values,
@@ -176,6 +177,9 @@ int fkt_plan_create(int n, int d, const double* x, const char* kernel, const cha
     po.threads = o.threads;
     po.hasDiagonal = o.has_diagonal != 0;
     po.diagonal = o.diagonal;
+    if (o.near_precision != 64 && o.near_precision != 32)
+      throw std::invalid_argument("near_precision must be 64 or 32");
+    po.nearPrecision = o.near_precision;
     if (po.p > fktb::kMaxExpansionOrder)
       throw OrderTooLarge("expansion order " + std::to_string(po.p) + " exceeds the supported cap " +
                           std::to_string(fktb::kMaxExpansionOrder));
@@ -259,7 +263,7 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
         FKTB_CUDA(cudaMemsetAsync(p.dMoments.get(), 0, static_cast<size_t>(p.tree->nodes) * p.P * nrhs * sizeof(double), st));
         break;
       case 1: fktb::launchS2M(p, p.dYp.get(), p.dMoments.get(), nrhs, st); break;
-      case 2: fktb::launchNear(p, p.dYp.get(), p.dZp.get(), nrhs, st); break;
+      case 2: fktb::launchNearAny(p, p.dYp.get(), p.dZp.get(), nrhs, st); break;
       case 3: fktb::launchM2T(p, p.dMoments.get(), p.dZp.get(), nrhs, st); break;
       case 4: fktb::launchScatterZ(p, p.dZp.get(), z_dev, nrhs, st); break;
       default: throw std::invalid_argument("stage must be 0..4");

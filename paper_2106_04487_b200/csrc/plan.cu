@@ -214,6 +214,11 @@ void destroyPlan(DevicePlan* plan) {
   if (st) cudaStreamDestroy(st);
 }
 
+void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
+  if (plan.options.nearPrecision == 32 && launchNear32(plan, yp, zp, nrhs, st)) return;
+  launchNear(plan, yp, zp, nrhs, st);
+}
+
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
   ensureWorkspace(plan, nrhs);
   const size_t n = static_cast<size_t>(plan.n);
@@ -221,7 +226,7 @@ void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cuda
   FKTB_CUDA(cudaMemsetAsync(plan.dZp.get(), 0, n * nrhs * sizeof(double), st));
   FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double), st));
   launchS2M(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, st);
-  launchNear(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
+  launchNearAny(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
   launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, st);
   launchScatterZ(plan, plan.dZp.get(), z, nrhs, st);
 }

@@ -110,6 +110,7 @@ struct PlanOptions {
   int threads = 0;
   bool hasDiagonal = false;
   double diagonal = 0.0;
+  int nearPrecision = 64;  // 64: FP64 near field; 32: FP32 fast mode (near32.cu)
 };
 
 struct DevicePlan {
@@ -148,6 +149,9 @@ const double* expTableDevice();
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+// FP32 fast mode when requested and available for (kernel, d), else FP64.
+void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void launchS2M(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
 void launchM2T(const DevicePlan& plan, const double* moments, double* zp, int nrhs, cudaStream_t stream);
 void launchGatherY(const DevicePlan& plan, const double* y, double* yp, int nrhs, cudaStream_t stream);
