@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_math.cuh"
@@ -151,8 +152,14 @@ void buildTiles(DevicePlan& plan) {
   upload(plan.dS2mTiles, plan.s2mTilesHost);
 }
 
+void clearGraphs(DevicePlan& plan) {
+  for (auto& kv : plan.graphs) cudaGraphExecDestroy(kv.second);
+  plan.graphs.clear();
+}
+
 void ensureWorkspace(DevicePlan& plan, int nrhs) {
   if (nrhs <= plan.nrhsCap) return;
+  clearGraphs(plan);
   const size_t n = static_cast<size_t>(plan.n);
   plan.dYp.resize(n * nrhs);
   plan.dZp.resize(n * nrhs);
@@ -189,6 +196,9 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     throw std::invalid_argument("unsupported on the GPU path: (d, p) too large for the runtime far-field kernels");
 
   FKTB_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+  FKTB_CUDA(cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking));
+  FKTB_CUDA(cudaEventCreateWithFlags(&plan->evGather, cudaEventDisableTiming));
+  FKTB_CUDA(cudaEventCreateWithFlags(&plan->evFar, cudaEventDisableTiming));
   plan->tree = std::make_unique<DeviceTree>();
   buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
   computeSetsGpu(*plan->tree, options.theta);
@@ -201,6 +211,8 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
+  (void)expTableDevice();  // lazy device table: initialise outside any graph capture
+  if (const char* g = std::getenv("FKTB_GRAPHS")) plan->useGraphs = std::atoi(g) != 0;
   FKTB_CUDA(cudaStreamSynchronize(plan->stream));
   plan->planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return plan;
@@ -209,9 +221,15 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
 void destroyPlan(DevicePlan* plan) {
   if (!plan) return;
   if (plan->stream) cudaStreamSynchronize(plan->stream);
-  cudaStream_t st = plan->stream;
+  if (plan->side) cudaStreamSynchronize(plan->side);
+  cudaStream_t st = plan->stream, side = plan->side;
+  cudaEvent_t e0 = plan->evGather, e1 = plan->evFar;
+  clearGraphs(*plan);
   delete plan;
   if (st) cudaStreamDestroy(st);
+  if (side) cudaStreamDestroy(side);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
 }
 
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
@@ -219,16 +237,53 @@ void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrh
   launchNear(plan, yp, zp, nrhs, st);
 }
 
-void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
-  ensureWorkspace(plan, nrhs);
+namespace {
+void enqueueMultiply(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
   const size_t n = static_cast<size_t>(plan.n);
+  // stream st: gather -> zero z -> near ------------------------> scatter
+  // side:                        \-> zero moments -> S2M -> M2T -/
   launchGatherY(plan, y, plan.dYp.get(), nrhs, st);
   FKTB_CUDA(cudaMemsetAsync(plan.dZp.get(), 0, n * nrhs * sizeof(double), st));
-  FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double), st));
-  launchS2M(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, st);
+  FKTB_CUDA(cudaEventRecord(plan.evGather, st));
+  FKTB_CUDA(cudaStreamWaitEvent(plan.side, plan.evGather, 0));
+  FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double),
+                            plan.side));
+  launchS2M(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
   launchNearAny(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
-  launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, st);
+  launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, plan.side);
+  FKTB_CUDA(cudaEventRecord(plan.evFar, plan.side));
+  FKTB_CUDA(cudaStreamWaitEvent(st, plan.evFar, 0));
   launchScatterZ(plan, plan.dZp.get(), z, nrhs, st);
+}
+}  // namespace
+
+void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
+  ensureWorkspace(plan, nrhs);
+  // The legacy default stream cannot be captured: run eagerly there.
+  if (!plan.useGraphs || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+    enqueueMultiply(plan, y, z, nrhs, st);
+    return;
+  }
+  const auto key = std::make_tuple(static_cast<const void*>(y), static_cast<const void*>(z), nrhs, st);
+  auto it = plan.graphs.find(key);
+  if (it == plan.graphs.end()) {
+    cudaGraph_t graph = nullptr;
+    FKTB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueueMultiply(plan, y, z, nrhs, st);
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    FKTB_CUDA(cudaStreamEndCapture(st, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    FKTB_CUDA(e);
+    it = plan.graphs.emplace(key, exec).first;
+  }
+  FKTB_CUDA(cudaGraphLaunch(it->second, st));
 }
 
 }  // namespace fktb

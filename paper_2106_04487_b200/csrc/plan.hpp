@@ -8,8 +8,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -136,6 +138,13 @@ struct DevicePlan {
   double planSeconds = 0.0;
   std::mutex mutex;                       // multiply() is serialised per plan
   cudaStream_t stream = nullptr;
+  // Far-field side stream: S2M -> M2T run concurrently with the near field.
+  cudaStream_t side = nullptr;
+  cudaEvent_t evGather = nullptr, evFar = nullptr;
+  // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
+  // on repeat calls (launch-bound small problems). Cleared on reallocation.
+  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
+  bool useGraphs = true;
 };
 
 std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
