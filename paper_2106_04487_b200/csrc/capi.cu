@@ -262,7 +262,7 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
         FKTB_CUDA(cudaMemsetAsync(p.dZp.get(), 0, static_cast<size_t>(p.n) * nrhs * sizeof(double), st));
         FKTB_CUDA(cudaMemsetAsync(p.dMoments.get(), 0, static_cast<size_t>(p.tree->nodes) * p.P * nrhs * sizeof(double), st));
         break;
-      case 1: fktb::launchS2M(p, p.dYp.get(), p.dMoments.get(), nrhs, st); break;
+      case 1: fktb::launchS2MAny(p, p.dYp.get(), p.dMoments.get(), nrhs, st); break;
       case 2: fktb::launchNearAny(p, p.dYp.get(), p.dZp.get(), nrhs, st); break;
       case 3: fktb::launchM2T(p, p.dMoments.get(), p.dZp.get(), nrhs, st); break;
       case 4: fktb::launchScatterZ(p, p.dZp.get(), z_dev, nrhs, st); break;

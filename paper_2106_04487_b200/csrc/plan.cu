@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "device_math.cuh"
+#include "moments.hpp"
 #include "plan.hpp"
 
 namespace fktb {
@@ -116,6 +117,7 @@ void buildFarParams(DevicePlan& plan) {
     }
   }
   cudaStream_t st = plan.stream;
+  plan.hscaleHost = hscale;
   plan.dHScale.resize(hscale.size());
   plan.dChainG.resize(cg.size());
   plan.dChainC.resize(cc.size());
@@ -157,9 +159,61 @@ void clearGraphs(DevicePlan& plan) {
   plan.graphs.clear();
 }
 
+template <class T>
+void uploadVec(DeviceBuffer<T>& dst, const std::vector<T>& src, cudaStream_t st) {
+  dst.resize(std::max<size_t>(1, src.size()));
+  if (!src.empty()) FKTB_CUDA(cudaMemcpyAsync(dst.get(), src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+// Tables, leaf tiles and the depth-ordered internal nodes of the monomial S2M.
+void buildMomentPlan(DevicePlan& plan) {
+  const DeviceTree& t = *plan.tree;
+  const int d = plan.d, p = plan.options.p;
+  MomentTables mt = buildMomentTables(d, p, *plan.harmonics, plan.factors, plan.compressed, plan.hscaleHost);
+  plan.monoCount = mt.count;
+  cudaStream_t st = plan.stream;
+  uploadVec(plan.dMomT, mt.T, st);
+  uploadVec(plan.dShiftOff, mt.off, st);
+  uploadVec(plan.dShiftB, mt.b, st);
+  uploadVec(plan.dShiftG, mt.g, st);
+  uploadVec(plan.dShiftCoef, mt.coef, st);
+  const MonomialBasis B(d, p);
+  std::vector<int> exps;
+  for (const auto& e : B.exps) exps.insert(exps.end(), e.begin(), e.end());
+  uploadVec(plan.dMonoExps, exps, st);
+  // leaves -> p2m tiles; depth of every node (pre-order, parents first)
+  std::vector<int> depth(static_cast<size_t>(t.nodes), 0);
+  int maxDepth = 0;
+  plan.p2mTilesHost.clear();
+  plan.farNodesHost.clear();
+  for (int b = 0; b < t.nodes; ++b) {
+    if (t.left[static_cast<size_t>(b)] >= 0) {
+      depth[static_cast<size_t>(t.left[static_cast<size_t>(b)])] = depth[static_cast<size_t>(b)] + 1;
+      depth[static_cast<size_t>(t.right[static_cast<size_t>(b)])] = depth[static_cast<size_t>(b)] + 1;
+    } else {
+      for (long long s = t.begin[static_cast<size_t>(b)]; s < t.end[static_cast<size_t>(b)]; s += 4096)
+        plan.p2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(4096, t.end[static_cast<size_t>(b)] - s)), s});
+    }
+    maxDepth = std::max(maxDepth, depth[static_cast<size_t>(b)]);
+    if (t.farOff[static_cast<size_t>(b) + 1] > t.farOff[static_cast<size_t>(b)]) plan.farNodesHost.push_back(b);
+  }
+  std::vector<int> levelNodes;
+  plan.levelOff.assign(1, 0);
+  for (int lv = 0; lv <= maxDepth; ++lv) {
+    for (int b = 0; b < t.nodes; ++b)
+      if (depth[static_cast<size_t>(b)] == lv && t.left[static_cast<size_t>(b)] >= 0) levelNodes.push_back(b);
+    plan.levelOff.push_back(static_cast<int>(levelNodes.size()));
+  }
+  uploadVec(plan.dLevelNodes, levelNodes, st);
+  uploadVec(plan.dFarNodes, plan.farNodesHost, st);
+  uploadVec(plan.dP2mTiles, plan.p2mTilesHost, st);
+  plan.useMoments = true;
+}
+
 void ensureWorkspace(DevicePlan& plan, int nrhs) {
   if (nrhs <= plan.nrhsCap) return;
   clearGraphs(plan);
+  if (plan.useMoments) plan.dMono.resize(static_cast<size_t>(plan.tree->nodes) * plan.monoCount * nrhs);
   const size_t n = static_cast<size_t>(plan.n);
   plan.dYp.resize(n * nrhs);
   plan.dZp.resize(n * nrhs);
@@ -208,6 +262,10 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   plan->compressed = compress;
   buildFarParams(*plan);
   buildTiles(*plan);
+  {
+    const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
+    if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
+  }
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
@@ -232,6 +290,13 @@ void destroyPlan(DevicePlan* plan) {
   if (e1) cudaEventDestroy(e1);
 }
 
+void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t st) {
+  if (plan.useMoments)
+    launchS2MMoments(plan, yp, moments, nrhs, st);
+  else
+    launchS2M(plan, yp, moments, nrhs, st);
+}
+
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
   if (plan.options.nearPrecision == 32 && launchNear32(plan, yp, zp, nrhs, st)) return;
   launchNear(plan, yp, zp, nrhs, st);
@@ -248,7 +313,7 @@ void enqueueMultiply(DevicePlan& plan, const double* y, double* z, int nrhs, cud
   FKTB_CUDA(cudaStreamWaitEvent(plan.side, plan.evGather, 0));
   FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double),
                             plan.side));
-  launchS2M(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
+  launchS2MAny(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
   launchNearAny(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
   launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, plan.side);
   FKTB_CUDA(cudaEventRecord(plan.evFar, plan.side));

@@ -141,6 +141,16 @@ struct DevicePlan {
   // Far-field side stream: S2M -> M2T run concurrently with the near field.
   cudaStream_t side = nullptr;
   cudaEvent_t evGather = nullptr, evFar = nullptr;
+  // Monomial-moment S2M (moments.cu) for the compile-time shapes.
+  bool useMoments = false;
+  int monoCount = 0;
+  std::vector<double> hscaleHost;
+  DeviceBuffer<double> dMono, dMomT, dShiftCoef;
+  DeviceBuffer<int> dShiftOff, dShiftB, dShiftG, dMonoExps, dLevelNodes, dFarNodes;
+  std::vector<FktbTile> p2mTilesHost;
+  DeviceBuffer<FktbTile> dP2mTiles;
+  std::vector<int> levelOff;     // internal nodes grouped by depth: [levelOff[l], levelOff[l+1])
+  std::vector<int> farNodesHost; // nodes with a non-empty far set
   // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
   // on repeat calls (launch-bound small problems). Cleared on reallocation.
   std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
@@ -162,6 +172,10 @@ bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs
 // FP32 fast mode when requested and available for (kernel, d), else FP64.
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void launchS2M(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
+bool momentsSupported(int d, int p);
+void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
+// Monomial-moment S2M when the plan has it, else the direct S2M.
+void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
 void launchM2T(const DevicePlan& plan, const double* moments, double* zp, int nrhs, cudaStream_t stream);
 void launchGatherY(const DevicePlan& plan, const double* y, double* yp, int nrhs, cudaStream_t stream);
 void launchScatterZ(const DevicePlan& plan, const double* zp, double* z, int nrhs, cudaStream_t stream);
