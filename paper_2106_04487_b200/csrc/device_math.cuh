@@ -315,6 +315,22 @@ constexpr int harmonic_count(int d, int p) {
   return h;
 }
 
+// Exponent window of the compressed target factors F_ki(r) for the builtin
+// recurrence kernels (derived from q in K' = q K, expansion.cpp:179-212):
+// inverse powers and constant q give r^-j (j <= p); gaussian gives [-p, p].
+constexpr int compressed_window_lo(int kid, int p) {
+  return kid == FKTB_KERNEL_GAUSSIAN || kid == FKTB_KERNEL_INVERSE_R || kid == FKTB_KERNEL_INVERSE_R2 ||
+                 kid == FKTB_KERNEL_INVERSE_R3 || kid == FKTB_KERNEL_EXPONENTIAL || kid == FKTB_KERNEL_MATERN12
+             ? -p
+             : -2 * p;
+}
+constexpr int compressed_window_hi(int kid, int p) {
+  return kid == FKTB_KERNEL_INVERSE_R || kid == FKTB_KERNEL_INVERSE_R2 || kid == FKTB_KERNEL_INVERSE_R3 ||
+                 kid == FKTB_KERNEL_EXPONENTIAL || kid == FKTB_KERNEL_MATERN12
+             ? 0
+             : p;
+}
+
 constexpr int harmonic_offset(int d, int k) {
   int h = 0;
   for (int q = 0; q < k; ++q) h += harmonic_count_deg(d, q);

@@ -66,6 +66,11 @@ typedef struct FktbFarParams {
   // Compressed factors (reference expansion.cpp:190-243): factor f = fOff[k]+i
   // target Laurent sum_{e=fLo..fHi} fc[fAt[f] + e - fLo] r^e (multiplies K(r)),
   // source polynomial sum_{e=gLo..gHi} fc[gAt[f] + e - gLo] r'^e.
+  // Dense target-factor windows (compile-time exponent range per kernel, see
+  // compressed_window in device_math.cuh): factor f, power e in [denseLo,
+  // denseHi] at fc[denseAt + f * (denseHi - denseLo + 1) + e - denseLo];
+  // denseAt < 0 when the factors do not fit (runtime loops are used then).
+  int denseLo, denseHi, denseAt;
   int fOff[FKTB_MAX_P + 2];
   int fLo[FKTB_FACTOR_MAX], fHi[FKTB_FACTOR_MAX], fAt[FKTB_FACTOR_MAX];
   int gLo[FKTB_FACTOR_MAX], gHi[FKTB_FACTOR_MAX], gAt[FKTB_FACTOR_MAX];

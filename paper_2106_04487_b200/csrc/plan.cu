@@ -98,6 +98,26 @@ void buildFarParams(DevicePlan& plan) {
       }
     }
     fp->fOff[p + 1] = f;
+    // dense windows (see compressed_window_lo/hi)
+    fp->denseLo = compressed_window_lo(plan.kernel.id, p);
+    fp->denseHi = compressed_window_hi(plan.kernel.id, p);
+    const int span = fp->denseHi - fp->denseLo + 1;
+    bool fits = c + f * span <= FKTB_FACTOR_CAP;
+    for (int k = 0; k <= p && fits; ++k)
+      for (const Laurent& F : plan.factors[static_cast<size_t>(k)].target)
+        if (F.minPower() < fp->denseLo || F.maxPower() > fp->denseHi) fits = false;
+    fp->denseAt = -1;
+    if (fits) {
+      fp->denseAt = c;
+      for (int k = 0; k <= p; ++k) {
+        const RadialFactor& rf = plan.factors[static_cast<size_t>(k)];
+        for (int i = 0; i < rf.rank; ++i) {
+          const int fi = fp->fOff[k] + i;
+          for (int e = fp->denseLo; e <= fp->denseHi; ++e)
+            fp->fc[fp->denseAt + fi * span + e - fp->denseLo] = toDouble(rf.target[static_cast<size_t>(i)].coeff(e));
+        }
+      }
+    }
   }
   plan.P = fp->P;
   plan.H = fp->H;
