@@ -348,6 +348,23 @@ constexpr int coef_offset(int d, int p, int k) {
   return c;
 }
 
+// Monic-scaled homogeneous Gegenbauer recurrence. The reference's
+// t^n C_n^(lambda)(x/t) (harmonics.cpp:212-230) satisfies
+//   g_n = a_n x g_{n-1} - b_n t^2 g_{n-2},  a_n = (2n+2lam-2)/n, b_n = (n+2lam-2)/n;
+// with g_n = kappa_n gh_n, kappa_n = a_1 ... a_n, the scaled values obey
+//   gh_n = x gh_{n-1} - beta_n t^2 gh_{n-2},  beta_n = b_n / (a_n a_{n-1}),
+// one multiply fewer per entry. The per-harmonic product of the kappas is
+// folded into the node moments on the host (plan.cu, moments.cpp).
+constexpr double gegen_a(int twoLam, int n) { return static_cast<double>(2 * n + twoLam - 2) / n; }
+constexpr double gegen_beta(int twoLam, int n) {
+  return (static_cast<double>(n + twoLam - 2) / n) / (gegen_a(twoLam, n) * gegen_a(twoLam, n - 1));
+}
+constexpr double gegen_kappa(int twoLam, int n) {
+  double k = 1.0;
+  for (int i = 1; i <= n; ++i) k *= gegen_a(twoLam, i);
+  return k;
+}
+
 // Per-level Gegenbauer table g[level][m][n], n <= P - m: flat offset.
 constexpr int g_level_size(int P) { return (P + 1) * (P + 2) / 2; }
 constexpr int g_index(int P, int level, int m, int n) {
@@ -501,12 +518,10 @@ __device__ __forceinline__ void harmonics_raw(const double (&x)[D], double r, do
         const int twoLam = D - 1 - level + 2 * m;  // 2 * lambda
         double* row = g + g_index(P, level, m, 0);
         row[0] = 1.0;
-        if (P - m >= 1) row[1] = static_cast<double>(twoLam) * xx;
+        if (P - m >= 1) row[1] = xx;
 #pragma unroll
         for (int n = 2; n <= P - m; ++n)
-          row[n] = (static_cast<double>(2 * n + twoLam - 2) * xx * row[n - 1] -
-                    static_cast<double>(n + twoLam - 2) * t2 * row[n - 2]) *
-                   (1.0 / n);
+          row[n] = fma(-gegen_beta(twoLam, n) * t2, row[n - 2], xx * row[n - 1]);
       }
     }
     chain_degrees<D, P, 0>(g, cA, cB, Y);

@@ -123,13 +123,19 @@ void buildFarParams(DevicePlan& plan) {
   plan.H = fp->H;
 
   // Per-harmonic fold Z_k * nrm_h^2 and the runtime chain table.
-  std::vector<double> hscale(static_cast<size_t>(fp->H));
+  std::vector<double> hscale(static_cast<size_t>(fp->H)), kappaHost(static_cast<size_t>(fp->H), 1.0);
   const int L = d > 2 ? d - 2 : 0;
   std::vector<int> cg(static_cast<size_t>(std::max(1, fp->H * L))), cc(static_cast<size_t>(fp->H)), ph(static_cast<size_t>(fp->H));
   for (int k = 0; k <= p; ++k) {
     int h = fp->hOff[k];
     for (const HarmonicChain& ch : hs.chains(k)) {
-      hscale[static_cast<size_t>(h)] = hs.z(k) * ch.norm * ch.norm;
+      // Z_k nrm^2 times kappa^2 for the monic-scaled Gegenbauer chains
+      // evaluated on both sides (device_math.cuh gegen_kappa)
+      double kappa = 1.0;
+      for (int l = 1; l <= L; ++l)
+        kappa *= gegen_kappa(d - 1 - l + 2 * ch.m[static_cast<size_t>(l)], ch.m[static_cast<size_t>(l - 1)] - ch.m[static_cast<size_t>(l)]);
+      kappaHost[static_cast<size_t>(h)] = kappa;
+      hscale[static_cast<size_t>(h)] = hs.z(k) * ch.norm * ch.norm * kappa * kappa;
       for (int l = 1; l <= L; ++l) cg[static_cast<size_t>(h * L + l - 1)] = g_index(p, l, ch.m[static_cast<size_t>(l)], ch.m[static_cast<size_t>(l - 1)] - ch.m[static_cast<size_t>(l)]);
       cc[static_cast<size_t>(h)] = d == 2 ? k : ch.m[static_cast<size_t>(d - 2)];
       ph[static_cast<size_t>(h)] = ch.phase;
@@ -138,6 +144,7 @@ void buildFarParams(DevicePlan& plan) {
   }
   cudaStream_t st = plan.stream;
   plan.hscaleHost = hscale;
+  plan.kappaHost = kappaHost;
   plan.dHScale.resize(hscale.size());
   plan.dChainG.resize(cg.size());
   plan.dChainC.resize(cc.size());
@@ -189,7 +196,11 @@ void uploadVec(DeviceBuffer<T>& dst, const std::vector<T>& src, cudaStream_t st)
 void buildMomentPlan(DevicePlan& plan) {
   const DeviceTree& t = *plan.tree;
   const int d = plan.d, p = plan.options.p;
-  MomentTables mt = buildMomentTables(d, p, *plan.harmonics, plan.factors, plan.compressed, plan.hscaleHost);
+  // T maps monomial moments to sum_src Y_raw (unscaled solid harmonics); the
+  // device chains are monic-scaled by 1/kappa, so rows carry hscale/kappa.
+  std::vector<double> rowScale(plan.hscaleHost.size());
+  for (size_t h = 0; h < rowScale.size(); ++h) rowScale[h] = plan.hscaleHost[h] / plan.kappaHost[h];
+  MomentTables mt = buildMomentTables(d, p, *plan.harmonics, plan.factors, plan.compressed, rowScale);
   plan.monoCount = mt.count;
   cudaStream_t st = plan.stream;
   uploadVec(plan.dMomT, mt.T, st);

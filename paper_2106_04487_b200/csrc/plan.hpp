@@ -144,7 +144,7 @@ struct DevicePlan {
   // Monomial-moment S2M (moments.cu) for the compile-time shapes.
   bool useMoments = false;
   int monoCount = 0;
-  std::vector<double> hscaleHost;
+  std::vector<double> hscaleHost, kappaHost;
   DeviceBuffer<double> dMono, dMomT, dShiftCoef;
   DeviceBuffer<int> dShiftOff, dShiftB, dShiftG, dMonoExps, dLevelNodes, dFarNodes;
   std::vector<FktbTile> p2mTilesHost;
