@@ -9,6 +9,7 @@
 // loop is FP64-pipe bound.
 #include "device_math.cuh"
 #include "fastmath.cuh"
+#include "near_common.cuh"
 #include "plan.hpp"
 
 #include <cmath>
@@ -107,51 +108,6 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constan
 // kernel length scale (and weights by its prefactor) so the pair body is the
 // canonical kernel; FP64 fast math (fastmath.cuh); 4 targets per thread
 // against AoS shared-memory sources read with 128-bit broadcast loads.
-
-template <int KID>
-struct FastKernel {
-  static constexpr bool supported =
-      KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
-      KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN ||
-      KID == FKTB_KERNEL_INVERSE_R || KID == FKTB_KERNEL_INVERSE_R2;
-  static constexpr bool needsTable =
-      KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
-      KID == FKTB_KERNEL_GAUSSIAN;
-  // canonical K at scaled squared distance q (> 0 unless the select handles 0)
-  template <int REP>
-  __device__ static __forceinline__ double eval(double q, const double* tab) {
-    if constexpr (KID == FKTB_KERNEL_MATERN32) {
-      const double u = sqrt_nr(q);
-      const double e = exp_neg<REP>(u, tab);
-      return fma(u, e, e);
-    } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
-      return exp_neg<REP>(sqrt_nr(q), tab);
-    } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
-      return rcp_nr(1.0 + q);
-    } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
-      return rsqrt_nr(1.0 + q);
-    } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return exp_neg<REP>(q, tab);
-    } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
-      return rsqrt_nr(q);
-    } else {
-      return rcp_nr(q);
-    }
-  }
-};
-
-// (scale for coordinates, prefactor for weights)
-inline void fastScales(const FktbKernelDesc& k, double& sc, double& wf) {
-  sc = 1.0;
-  wf = 1.0;
-  switch (k.id) {
-    case FKTB_KERNEL_MATERN32: sc = k.a; wf = k.s2; break;
-    case FKTB_KERNEL_MATERN12: sc = 1.0 / k.rho; wf = k.s2; break;
-    case FKTB_KERNEL_CAUCHY:
-    case FKTB_KERNEL_RATIONAL_QUADRATIC: sc = std::sqrt(k.is2); break;
-    default: break;
-  }
-}
 
 struct FastArgs {
   NearArgs a;

@@ -296,6 +296,11 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   {
     const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
+    // "1" enables the symmetric leaf-pair near field (nearsym.cu). Measured
+    // slower than the one-way kernel on cfg2-4 (padding of small T_AB row
+    // sets), so it stays an opt-in A/B knob.
+    const char* sym = std::getenv("FKTB_NEAR_SYM");
+    if (sym && std::string(sym) == "1") buildNearBlocks(*plan);
   }
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
@@ -330,6 +335,7 @@ void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int
 
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
   if (plan.options.nearPrecision == 32 && launchNear32(plan, yp, zp, nrhs, st)) return;
+  if (launchNearSym(plan, yp, zp, nrhs, st)) return;
   launchNear(plan, yp, zp, nrhs, st);
 }
 

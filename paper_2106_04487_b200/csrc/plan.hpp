@@ -151,6 +151,12 @@ struct DevicePlan {
   DeviceBuffer<FktbTile> dP2mTiles;
   std::vector<int> levelOff;     // internal nodes grouped by depth: [levelOff[l], levelOff[l+1])
   std::vector<int> farNodesHost; // nodes with a non-empty far set
+  // Symmetric near-field blocks (nearsym.cu).
+  bool nearSym = false;
+  DeviceBuffer<uint32_t> dNearPool;
+  std::vector<FktbBlockTile> blockTilesHost;
+  DeviceBuffer<FktbBlockTile> dBlockTiles;
+  long long symPairs = 0, oneWayPairs = 0;
   // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
   // on repeat calls (launch-bound small problems). Cleared on reallocation.
   std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
@@ -168,6 +174,8 @@ const double* expTableDevice();
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+void buildNearBlocks(DevicePlan& plan);
+bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 // FP32 fast mode when requested and available for (kernel, d), else FP64.
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
