@@ -12,11 +12,16 @@
 // atomic accumulation).
 //
 // Blocks are lists of permuted positions in one index pool:
-//   [ near-set positions (the CSR of K2) | identity 0..n-1 | complements ]
-// Tiles: <= 256 rows x all columns; columns are staged in shared memory
-// 512 at a time. In symmetric tiles each warp reduces its 128 pair values per
-// column with shuffles into a per-warp shared slot; the column sums go to z
-// with one atomic per column per tile.
+//   [ near-set positions (the CSR of K2) | identity 0..n-1 | extra lists ]
+// The extra lists are the complements A \ T_BA and, per leaf, the merged rows
+// that need all of the leaf's sources (non-mutual targets and the leaf's own),
+// so those form one long row list instead of many short ones.
+// Tiles: <= 256 rows x all columns. Warp w owns rows [128w, 128w + 128) in
+// groups of 32 (warp-uniform group count), so short row sets pad to 32, not
+// 256. Columns are staged in shared memory (512 at a time one-way, 32 in
+// symmetric tiles); in symmetric tiles every thread stores its per-column
+// partial to shared memory and the column sums go to z with one atomic per
+// column per tile.
 #include <algorithm>
 #include <unordered_map>
 
@@ -31,7 +36,7 @@ constexpr int kSymThreads = 64;
 constexpr int kSymTPT = 4;
 constexpr int kSymRows = kSymThreads * kSymTPT;
 constexpr int kSymChunk = 512;    // columns staged per pass, one-way tiles
-constexpr int kSymChunkS = 64;    // columns per pass in symmetric tiles
+constexpr int kSymChunkS = 32;    // columns per pass in symmetric tiles
 constexpr int kZsStride = kSymThreads + 1;
 
 struct SymArgs {
@@ -50,13 +55,17 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
                                            const double* tab) {
   constexpr int SP = (D + 2) / 2 * 2;
   const int n = A.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wRows = min(max(tile.rowCount - warp * 32 * kSymTPT, 0), 32 * kSymTPT);
+  const int groups = (wRows + 31) >> 5;  // warp-uniform
+  const int activeThreads = tile.rowCount > 32 * kSymTPT ? kSymThreads : 32;
   int tpos[kSymTPT];
   double tx[kSymTPT][D];
   double ty[kSymTPT];
   double acc[kSymTPT];
 #pragma unroll
   for (int i = 0; i < kSymTPT; ++i) {
-    const int idx = threadIdx.x + i * kSymThreads;
+    const int idx = warp * 32 * kSymTPT + i * 32 + lane;
     tpos[i] = idx < tile.rowCount ? static_cast<int>(A.pool[tile.rowOff + idx]) : -1;
     const int p = tpos[i] >= 0 ? tpos[i] : 0;
 #pragma unroll
@@ -76,7 +85,7 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
     }
     __syncthreads();
 #pragma unroll 2
-    for (int s = 0; s < cn; ++s) {
+    for (int s = 0; s < (groups > 0 ? cn : 0); ++s) {
       double src[SP];
 #pragma unroll
       for (int q = 0; q < SP; q += 2) {
@@ -87,6 +96,7 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
       double part = 0.0;
 #pragma unroll
       for (int i = 0; i < kSymTPT; ++i) {
+        if (i >= groups) break;
         const double d0 = tx[i][0] - src[0];
         double q = fma(d0, d0, kQBias);
 #pragma unroll
@@ -106,7 +116,7 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
       for (int s = threadIdx.x; s < cn; s += kSymThreads) {
         double t = 0.0;
 #pragma unroll 8
-        for (int j = 0; j < kSymThreads; ++j) t += zs[s * kZsStride + j];
+        for (int j = 0; j < activeThreads; ++j) t += zs[s * kZsStride + j];
         atomicAdd(A.zp + A.pool[tile.colOff + cs + s], t);
       }
     }
@@ -117,9 +127,9 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
 }
 
 template <int KID, int D, bool SEL>
-__global__ void __launch_bounds__(kSymThreads) near_block_kernel(const __grid_constant__ SymArgs A) {
+__global__ void __launch_bounds__(kSymThreads, 10) near_block_kernel(const __grid_constant__ SymArgs A) {
   constexpr int SP = (D + 2) / 2 * 2;
-  // one-way tiles: ss[512 * SP]; symmetric tiles: ss[64 * SP] then zs[64 x 65]
+  // one-way tiles: ss[512 * SP]; symmetric tiles: ss[32 * SP] then zs[32 x 65]
   constexpr int kOne = kSymChunk * SP, kSym = kSymChunkS * (SP + kZsStride);
   __shared__ __align__(16) double ss[kOne > kSym ? kOne : kSym];
   double* zs = ss + kSymChunkS * SP;
@@ -165,7 +175,7 @@ bool symSupported(int kid, int d) {
 
 }  // namespace
 
-void buildNearBlocks(DevicePlan& plan) {
+void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
   const DeviceTree& t = *plan.tree;
   if (!symSupported(plan.kernel.id, plan.d) || t.nearTotal == 0) return;
   const int n = t.n;
@@ -224,16 +234,22 @@ void buildNearBlocks(DevicePlan& plan) {
     if (t.left[static_cast<size_t>(A)] >= 0) continue;
     const long long aBegin = t.begin[static_cast<size_t>(A)];
     const int aCount = static_cast<int>(t.end[static_cast<size_t>(A)] - t.begin[static_cast<size_t>(A)]);
+    if (oneWayOnly) {  // A/B: the same kernel on the plain leaf decomposition
+      addBlock(t.nearOff[static_cast<size_t>(A)], static_cast<int>(t.nearOff[static_cast<size_t>(A) + 1] - t.nearOff[static_cast<size_t>(A)]),
+               identityBase + aBegin, aCount, 0);
+      continue;
+    }
+    // rows that need all of A's sources: A's own and non-mutual targets, merged
+    const long long fullBase = identityBase + n + static_cast<long long>(comp.size());
+    for (const auto& [B, sAB] : segsOf[static_cast<size_t>(A)])
+      if (B == A || seg.find(key(B, A)) == seg.end())
+        comp.insert(comp.end(), nearPos.begin() + sAB.off, nearPos.begin() + sAB.off + sAB.len);
+    addBlock(fullBase, static_cast<int>(identityBase + n + static_cast<long long>(comp.size()) - fullBase),
+             identityBase + aBegin, aCount, 0);
     for (const auto& [B, sAB] : segsOf[static_cast<size_t>(A)]) {
-      if (B == A) {
-        addBlock(sAB.off, sAB.len, identityBase + aBegin, aCount, 0);
-        continue;
-      }
+      if (B == A) continue;
       auto it = seg.find(key(B, A));
-      if (it == seg.end()) {
-        addBlock(sAB.off, sAB.len, identityBase + aBegin, aCount, 0);
-        continue;
-      }
+      if (it == seg.end()) continue;
       if (A > B) continue;  // mutual pair handled once, from the smaller leaf id
       const Seg& sBA = it->second;  // rows in A that need B's sources
       const long long bBegin = t.begin[static_cast<size_t>(B)];

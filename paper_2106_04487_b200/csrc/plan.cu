@@ -300,7 +300,7 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     // slower than the one-way kernel on cfg2-4 (padding of small T_AB row
     // sets), so it stays an opt-in A/B knob.
     const char* sym = std::getenv("FKTB_NEAR_SYM");
-    if (sym && std::string(sym) == "1") buildNearBlocks(*plan);
+    if (sym && (std::string(sym) == "1" || std::string(sym) == "2")) buildNearBlocks(*plan, std::string(sym) == "2");
   }
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));

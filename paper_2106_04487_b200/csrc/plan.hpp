@@ -174,7 +174,7 @@ const double* expTableDevice();
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
-void buildNearBlocks(DevicePlan& plan);
+void buildNearBlocks(DevicePlan& plan, bool oneWayOnly = false);
 bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 // FP32 fast mode when requested and available for (kernel, d), else FP64.

@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_nearsym.py -q -x 2>&1 | tail -3
-timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 600 python bench.py --steps 10 --warmup 3 2>&1 | tail -1
+for c in 2 3; do for m in 1 2; do echo "cfg$c sym=$m"; FKTB_NEAR_SYM=$m SWEEP_CFG=$c python scripts/sweep_near.py 0; done; done
