@@ -11,8 +11,10 @@ K back-to-back device multiplies on the launching stream, max over ranks);
 MVM -> D2H z every step). The roofline is for the dominant kernel (near
 field K3, FP64-pipe bound) against the FP64 FMA peak measured live on this
 GPU. The reference arm times the unmodified reference FKT (oracle/_ref) on
-the host cores. Multi-GPU: independent replicas per rank ("replicas only",
-DESIGN.md §6), scaling "weak".
+the host cores. Multi-GPU (torchrun, N ranks): ONE MVM per step sharded by
+target over the ranks (paper_2106_04487_b200.distributed.ShardedPlan: partial
+moments -> NCCL all-reduce -> near + M2T of the owned targets -> NCCL
+all-reduce of z), scaling "strong" (total work fixed), DESIGN.md §6.
 """
 import argparse
 import json
@@ -117,11 +119,19 @@ def dist_setup():
     return world, rank, local
 
 
-def near_evals(tree) -> int:
-    off, _ = tree.nearCsr()
-    counts = np.diff(off)
+def near_evals(tree, lo=None, hi=None) -> int:
+    """Kernel evaluations of the near field; with [lo, hi), only the targets at
+    those tree positions (one shard)."""
+    off, idx = tree.nearCsr()
     sizes = tree.ends.astype(np.int64) - tree.begins.astype(np.int64)
-    return int(np.sum(counts * sizes))
+    if lo is None:
+        return int(np.sum(np.diff(off) * sizes))
+    order = tree.order().astype(np.int64)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(order.size)
+    tp = inv[idx.astype(np.int64)]
+    w = np.repeat(sizes, np.diff(off))
+    return int(w[(tp >= lo) & (tp < hi)].sum())
 
 
 def s2m_pairs(tree) -> int:
@@ -163,7 +173,12 @@ def run_ours(args):
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[args.cfg]
     n, nrhs = c["n"], c["nrhs"]
@@ -180,27 +195,37 @@ def run_ours(args):
     # CUDA graph on first use and replays it (same kernels, fewer launches).
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    if sharded:
+        from paper_2106_04487_b200.distributed import ShardedPlan
+
+        sp = ShardedPlan(pl)
+
+        def mul():
+            sp.multiply_device(ydev, zdev, stream=stream)
+    else:
+        def mul():
+            pl.multiply_device(ydev, zdev, stream=stream)
     for _ in range(args.warmup):
-        pl.multiply_device(ydev, zdev, stream=stream)
+        mul()
     torch.cuda.synchronize()
     zhost = zdev.cpu().numpy()
     parity = golden_parity(args.cfg, zhost.T if nrhs > 1 else zhost) if rank == 0 else None
 
     # ---- timed region: K device multiplies -------------------------------
     with ClockSampler(local) as clocks:
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            pl.multiply_device(ydev, zdev, stream=stream)
+            mul()
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -224,25 +249,34 @@ def run_ours(args):
     zh = torch.empty_like(yh).pin_memory()
     import ctypes as C
 
-    def host_mul():
-        rc = fkt.lib.fkt_plan_multiply(pl._h, C.cast(C.c_void_p(yh.data_ptr()), C.POINTER(C.c_double)),
-                                       C.cast(C.c_void_p(zh.data_ptr()), C.POINTER(C.c_double)), nrhs)
-        fkt._check(rc)
+    if sharded:
+        def host_mul():  # pinned y -> H2D -> sharded MVM (all of z on every rank) -> D2H z
+            ydev.copy_(yh.reshape(ydev.shape), non_blocking=True)
+            mul()
+            zh.reshape(zdev.shape).copy_(zdev, non_blocking=True)
+            stream.synchronize()
+    else:
+        def host_mul():
+            rc = fkt.lib.fkt_plan_multiply(pl._h, C.cast(C.c_void_p(yh.data_ptr()), C.POINTER(C.c_double)),
+                                           C.cast(C.c_void_p(zh.data_ptr()), C.POINTER(C.c_double)), nrhs)
+            fkt._check(rc)
 
     for _ in range(max(1, args.warmup // 2)):
         host_mul()
-    if world > 1:
+    if sharded:
         dist.barrier()
     te = time.perf_counter()
     e2e_steps = max(3, args.steps // 2)
     for _ in range(e2e_steps):
         host_mul()
     e2e_s = (time.perf_counter() - te) / e2e_steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    launches = int(fkt.lib.fkt_plan_kernel_launches(pl._h, nrhs))
+    shard_lo, shard_hi = pl.shard_range()
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -252,7 +286,8 @@ def run_ours(args):
     fkt._check(fkt.lib.fkt_fma_peak(0, C.byref(peak)))
     peak_tf = peak.value / 1e12
     tree = pl.tree()
-    nev = near_evals(tree)
+    nev_all = near_evals(tree)
+    nev = near_evals(tree, shard_lo, shard_hi) if sharded else nev_all  # rank 0's near launch
     fpp = near_flops_per_pair(c["kernel"], c["d"]) + 2 * (nrhs - 1)
     near_flops = nev * fpp
     P = info["coefficient_count"]
@@ -261,7 +296,7 @@ def run_ours(args):
     near_ms = stage_ms[2]
     achieved = near_flops / (near_ms * 1e-3) / 1e12
     mvm_s = ms * 1e-3
-    value = world * 1.0 / mvm_s
+    value = 1.0 / mvm_s  # one MVM per step for the whole job
     line = {
         "metric": METRIC,
         "value": value,
@@ -271,20 +306,21 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64" if args.near_precision == 64 else "f64 (near field f32 fast mode)",
         "data": "synthetic (SURVEY Appendix B recipe, fkt::Rng(42); no public dataset)",
         "config": {
             "workload": workload_desc(args.cfg),
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"target-sharded x{world} (moment + z all-reduce over NCCL)" if sharded
+                            else "single GPU"),
             "l2": "inputs larger than L2: far lists %.0f MB + near lists %.0f MB + coordinates %.0f MB per step"
                   % (info["far_total"] * 4 / 1e6, info["near_total"] * 4 / 1e6, n * c["d"] * 8 / 1e6),
             "plan_seconds": plan_s,
             "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
-            "near_evals": nev, "coefficients": P,
+            "near_evals": nev_all, "coefficients": P,
         },
-        "effective_interactions_per_s": world * float(n) * n * nrhs / mvm_s,
+        "effective_interactions_per_s": float(n) * n * nrhs / mvm_s,
         "stage_ms": {"gather": stage_ms[0], "s2m": stage_ms[1], "near": stage_ms[2], "m2t": stage_ms[3],
                      "scatter": stage_ms[4]},
         "roofline": {
@@ -299,19 +335,22 @@ def run_ours(args):
             "traffic": traffic_for(args.cfg),
             "flops_per_launch": near_flops,
             "flops_per_pair": fpp,
-            "whole_step_frac": (near_flops + far_flops) / mvm_s / 1e12 / peak_tf,
+            "whole_step_frac": (nev_all * fpp + far_flops) / mvm_s / 1e12 / peak_tf / world,
         },
-        "e2e": {"value": world * 1.0 / e2e_s, "unit": "MVM/s", "h2d_bytes_per_step": int(yh.numel() * 8),
-                "d2h_bytes_per_step": int(zh.numel() * 8),
-                "method": "fkt_plan_multiply (C-ABI, pinned host y/z, H2D+MVM+D2H per step), wall clock"},
-        "gpu_launches": 5 * args.steps,
+        "e2e": {"value": 1.0 / e2e_s, "unit": "MVM/s", "h2d_bytes_per_step": int(yh.numel() * 8) * world,
+                "d2h_bytes_per_step": int(zh.numel() * 8) * world,
+                "method": ("ShardedPlan.multiply_device per rank (pinned host y -> H2D, sharded MVM, D2H of all z), "
+                           "wall clock, max over ranks" if sharded else
+                           "fkt_plan_multiply (C-ABI, pinned host y/z, H2D+MVM+D2H per step), wall clock")},
+        "gpu_launches": launches * args.steps,
+        "gpu_launches_per_step": launches,
         "clocks": clocks.summary(),
         "parity": parity,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cfg, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
@@ -402,6 +441,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the target-sharded multi-GPU path even at one rank (it is automatic for N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)

@@ -101,6 +101,27 @@ int fkt_plan_multiply_device(fkt_plan_t plan, const double* y_dev, double* z_dev
  * 0 gather, 1 s2m, 2 near, 3 m2t, 4 scatter (workspaces owned by the plan). */
 int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, double* z_dev, int nrhs, void* stream);
 
+/* Multi-GPU target sharding (replaces the node-chunked thread
+ * split of FktPlan::multiply, transform.cpp:18-35,184-204). Every rank holds
+ * the full plan and owns the contiguous, leaf-aligned, cost-balanced range
+ * [pos_lo, pos_hi) of tree positions. Under a shard, multiply computes
+ *   stage 1: partial node moments from the owned sources only,
+ *   stage 2/3: near and far interactions of the owned targets only,
+ * so z is exact on the owned targets and 0 elsewhere PROVIDED the moment
+ * tables were summed over all ranks between stages 1 and 3 (the one data-path
+ * exchange; fkt_plan_moments_device exposes the table, [rhs][node][P], count =
+ * nodes * P per right-hand side). shards = 1 restores the whole problem. */
+int fkt_plan_set_shard(fkt_plan_t plan, int shard, int shards);
+int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi);
+int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_per_rhs);
+/* How many of this library's kernels one multiply with nrhs right-hand sides
+ * launches on the current shard (memsets excluded); -1 on error. */
+long long fkt_plan_kernel_launches(fkt_plan_t plan, int nrhs);
+/* The cut rule (host only): leaves in position order with their end position
+ * and cumulative cost; cuts has shards+1 entries (cuts[0]=0, cuts[shards]=n). */
+int fkt_shard_cuts(const uint32_t* leaf_end, const unsigned long long* leaf_cum_cost, int leaves, int shards, uint32_t n,
+                   uint32_t* cuts);
+
 /* Tree view of a plan (borrowed; valid while the plan lives). */
 fkt_tree_t fkt_plan_tree(fkt_plan_t plan);
 

@@ -444,6 +444,32 @@ class FktPlan:
                                          C.c_void_p(z.data_ptr() if z is not None else 0), nrhs,
                                          C.c_void_p(st.cuda_stream)))
 
+    # ---- multi-GPU target sharding (see distributed.py) ----------
+    def set_shard(self, shard: int, shards: int) -> None:
+        """Own the cost-balanced, leaf-aligned target range `shard` of `shards`."""
+        _check(lib.fkt_plan_set_shard(self._h, int(shard), int(shards)))
+
+    def shard_range(self):
+        """Owned tree positions [lo, hi)."""
+        lo, hi = C.c_longlong(), C.c_longlong()
+        _check(lib.fkt_plan_shard_range(self._h, C.byref(lo), C.byref(hi)))
+        return int(lo.value), int(hi.value)
+
+    def moments_view(self, nrhs: int = 1):
+        """The plan's node-moment table ([rhs][node][P], float64) as a torch CUDA
+        tensor sharing its memory (valid until the next reallocation)."""
+        import torch
+
+        ptr, per = C.POINTER(C.c_double)(), C.c_longlong()
+        _check(lib.fkt_plan_moments_device(self._h, C.byref(ptr), C.byref(per)))
+        count = int(per.value) * int(nrhs)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "version": 3,
+                                        "data": (C.cast(ptr, C.c_void_p).value, False), "strides": None}
+
+        return torch.as_tensor(_View(), device="cuda")
+
 
 def plan(cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None) -> FktPlan:
     """fkt::plan (transform.cpp:206-208)."""

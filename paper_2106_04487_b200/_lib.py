@@ -86,6 +86,11 @@ SIGNATURES = {
     "fkt_plan_multiply": (C.c_int, C.c_void_p, _d, _d, C.c_int),
     "fkt_plan_multiply_device": (C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p),
     "fkt_plan_stage_device": (C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p),
+    "fkt_plan_set_shard": (C.c_int, C.c_void_p, C.c_int, C.c_int),
+    "fkt_plan_shard_range": (C.c_int, C.c_void_p, _ll, _ll),
+    "fkt_plan_moments_device": (C.c_int, C.c_void_p, C.POINTER(C.POINTER(C.c_double)), _ll),
+    "fkt_plan_kernel_launches": (C.c_longlong, C.c_void_p, C.c_int),
+    "fkt_shard_cuts": (C.c_int, _u32, C.POINTER(C.c_ulonglong), C.c_int, C.c_int, C.c_uint32, _u32),
     "fkt_plan_tree": (C.c_void_p, C.c_void_p),
     "fkt_tree_create": (C.c_int, C.c_int, C.c_int, _d, C.c_int, C.POINTER(C.c_void_p)),
     "fkt_tree_compute_sets": (C.c_int, C.c_void_p, C.c_double),

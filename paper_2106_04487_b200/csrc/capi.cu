@@ -254,7 +254,9 @@ int fkt_plan_multiply_device(fkt_plan_t plan, const double* y_dev, double* z_dev
 int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, double* z_dev, int nrhs, void* stream) {
   return guarded([&] {
     auto& p = *plan->plan;
-    if (nrhs > p.nrhsCap) throw std::invalid_argument("stage: run one multiply with this nrhs first");
+    if (nrhs < 1) throw DimensionMismatch("stage: nrhs must be >= 1");
+    if (stage == 0) fktb::ensureWorkspace(p, nrhs);
+    if (nrhs > p.nrhsCap) throw std::invalid_argument("stage: run stage 0 (or a multiply) with this nrhs first");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
     switch (stage) {
       case 0:
@@ -269,6 +271,45 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
       default: throw std::invalid_argument("stage must be 0..4");
     }
     if (!stream) FKTB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fkt_plan_set_shard(fkt_plan_t plan, int shard, int shards) {
+  return guarded([&] {
+    auto& p = *plan->plan;
+    std::lock_guard<std::mutex> lock(p.mutex);
+    fktb::setShard(p, shard, shards);
+  });
+}
+
+int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi) {
+  return guarded([&] {
+    *pos_lo = plan->plan->shardLo;
+    *pos_hi = plan->plan->shardHi;
+  });
+}
+
+int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_per_rhs) {
+  return guarded([&] {
+    *moments = plan->plan->dMoments.get();
+    *count_per_rhs = static_cast<long long>(plan->plan->tree->nodes) * plan->plan->P;
+  });
+}
+
+long long fkt_plan_kernel_launches(fkt_plan_t plan, int nrhs) {
+  long long out = -1;
+  guarded([&] { out = fktb::kernelLaunches(*plan->plan, std::max(1, nrhs)); });
+  return out;
+}
+
+int fkt_shard_cuts(const uint32_t* leaf_end, const unsigned long long* leaf_cum_cost, int leaves, int shards, uint32_t n,
+                   uint32_t* cuts) {
+  return guarded([&] {
+    if (shards < 1 || leaves < 0) throw std::invalid_argument("shard_cuts: shards >= 1, leaves >= 0");
+    std::vector<std::pair<uint32_t, unsigned long long>> le(static_cast<size_t>(leaves));
+    for (int i = 0; i < leaves; ++i) le[static_cast<size_t>(i)] = {leaf_end[i], leaf_cum_cost[i]};
+    const auto c = fktb::shardCutsFromLeaves(le, shards, n);
+    std::copy(c.begin(), c.end(), cuts);
   });
 }
 

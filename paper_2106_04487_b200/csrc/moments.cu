@@ -210,7 +210,7 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   const size_t perRhs = static_cast<size_t>(kP2MThreads) * C * sizeof(double);
   const int chunk = std::max(1, static_cast<int>((200 * 1024) / perRhs));
   const int tiles = static_cast<int>(plan.p2mTilesHost.size());
-  for (int r0 = 0; r0 < nrhs; r0 += chunk) {
+  for (int r0 = 0; r0 < nrhs && tiles > 0; r0 += chunk) {
     MomArgs B = A;
     B.nrhs = std::min(chunk, nrhs - r0);
     B.yp = yp + static_cast<size_t>(r0) * t.n;

@@ -156,19 +156,27 @@ void buildFarParams(DevicePlan& plan) {
   plan.far = std::move(fp);
 }
 
+// Work tiles over the lists; under a shard (shard.cu) only the owned targets'
+// sub-range of every list and the owned sources.
 void buildTiles(DevicePlan& plan) {
   const DeviceTree& t = *plan.tree;
   const int ft = farTileSize(), nt = nearTileSize();
   plan.farTilesHost.clear();
   plan.nearTilesHost.clear();
   plan.s2mTilesHost.clear();
+  const long long lo = plan.shardLo, hi = plan.shardHi;
   for (int b = 0; b < t.nodes; ++b) {
-    const long long f0 = t.farOff[static_cast<size_t>(b)], f1 = t.farOff[static_cast<size_t>(b) + 1];
+    const size_t B = static_cast<size_t>(b);
+    const bool farAny = t.farOff[B + 1] > t.farOff[B];
+    const long long f0 = plan.farSub.empty() ? t.farOff[B] : plan.farSub[2 * B];
+    const long long f1 = plan.farSub.empty() ? t.farOff[B + 1] : plan.farSub[2 * B + 1];
     for (long long s = f0; s < f1; s += ft) plan.farTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(ft, f1 - s)), s});
-    if (f1 > f0)
-      for (long long s = t.begin[static_cast<size_t>(b)]; s < t.end[static_cast<size_t>(b)]; s += kS2MTileSources)
-        plan.s2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(kS2MTileSources, t.end[static_cast<size_t>(b)] - s)), s});
-    const long long n0 = t.nearOff[static_cast<size_t>(b)], n1 = t.nearOff[static_cast<size_t>(b) + 1];
+    const long long s0 = std::max<long long>(t.begin[B], lo), s1 = std::min<long long>(t.end[B], hi);
+    if (farAny)
+      for (long long s = s0; s < s1; s += kS2MTileSources)
+        plan.s2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(kS2MTileSources, s1 - s)), s});
+    const long long n0 = plan.nearSub.empty() ? t.nearOff[B] : plan.nearSub[2 * B];
+    const long long n1 = plan.nearSub.empty() ? t.nearOff[B + 1] : plan.nearSub[2 * B + 1];
     for (long long s = n0; s < n1; s += nt) plan.nearTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(nt, n1 - s)), s});
   }
   auto upload = [&](DeviceBuffer<FktbTile>& dst, const std::vector<FktbTile>& src) {
@@ -192,6 +200,8 @@ void uploadVec(DeviceBuffer<T>& dst, const std::vector<T>& src, cudaStream_t st)
   if (!src.empty()) FKTB_CUDA(cudaMemcpyAsync(dst.get(), src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
 }
 
+void buildP2MTiles(DevicePlan& plan);
+
 // Tables, leaf tiles and the depth-ordered internal nodes of the monomial S2M.
 void buildMomentPlan(DevicePlan& plan) {
   const DeviceTree& t = *plan.tree;
@@ -212,18 +222,14 @@ void buildMomentPlan(DevicePlan& plan) {
   std::vector<int> exps;
   for (const auto& e : B.exps) exps.insert(exps.end(), e.begin(), e.end());
   uploadVec(plan.dMonoExps, exps, st);
-  // leaves -> p2m tiles; depth of every node (pre-order, parents first)
+  // depth of every node (pre-order, parents first)
   std::vector<int> depth(static_cast<size_t>(t.nodes), 0);
   int maxDepth = 0;
-  plan.p2mTilesHost.clear();
   plan.farNodesHost.clear();
   for (int b = 0; b < t.nodes; ++b) {
     if (t.left[static_cast<size_t>(b)] >= 0) {
       depth[static_cast<size_t>(t.left[static_cast<size_t>(b)])] = depth[static_cast<size_t>(b)] + 1;
       depth[static_cast<size_t>(t.right[static_cast<size_t>(b)])] = depth[static_cast<size_t>(b)] + 1;
-    } else {
-      for (long long s = t.begin[static_cast<size_t>(b)]; s < t.end[static_cast<size_t>(b)]; s += 4096)
-        plan.p2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(4096, t.end[static_cast<size_t>(b)] - s)), s});
     }
     maxDepth = std::max(maxDepth, depth[static_cast<size_t>(b)]);
     if (t.farOff[static_cast<size_t>(b) + 1] > t.farOff[static_cast<size_t>(b)]) plan.farNodesHost.push_back(b);
@@ -237,9 +243,25 @@ void buildMomentPlan(DevicePlan& plan) {
   }
   uploadVec(plan.dLevelNodes, levelNodes, st);
   uploadVec(plan.dFarNodes, plan.farNodesHost, st);
-  uploadVec(plan.dP2mTiles, plan.p2mTilesHost, st);
   plan.useMoments = true;
+  buildP2MTiles(plan);
 }
+
+// Leaf tiles of the monomial S2M over the owned sources.
+void buildP2MTiles(DevicePlan& plan) {
+  const DeviceTree& t = *plan.tree;
+  plan.p2mTilesHost.clear();
+  for (int b = 0; b < t.nodes; ++b) {
+    if (t.left[static_cast<size_t>(b)] >= 0) continue;
+    const long long s0 = std::max<long long>(t.begin[static_cast<size_t>(b)], plan.shardLo);
+    const long long s1 = std::min<long long>(t.end[static_cast<size_t>(b)], plan.shardHi);
+    for (long long s = s0; s < s1; s += 4096)
+      plan.p2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(4096, s1 - s)), s});
+  }
+  uploadVec(plan.dP2mTiles, plan.p2mTilesHost, plan.stream);
+}
+
+}  // namespace
 
 void ensureWorkspace(DevicePlan& plan, int nrhs) {
   if (nrhs <= plan.nrhsCap) return;
@@ -252,7 +274,14 @@ void ensureWorkspace(DevicePlan& plan, int nrhs) {
   plan.nrhsCap = nrhs;
 }
 
-}  // namespace
+void rebuildTiles(DevicePlan& plan) {
+  FKTB_CUDA(cudaStreamSynchronize(plan.stream));  // tiles may be in use by queued work
+  FKTB_CUDA(cudaStreamSynchronize(plan.side));
+  clearGraphs(plan);
+  buildTiles(plan);
+  if (plan.useMoments) buildP2MTiles(plan);
+  FKTB_CUDA(cudaStreamSynchronize(plan.stream));
+}
 
 std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
                                        const PlanOptions& options) {
@@ -260,6 +289,7 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   auto plan = std::make_unique<DevicePlan>();
   plan->n = n;
   plan->d = d;
+  plan->shardHi = static_cast<uint32_t>(n);
   plan->options = options;
   plan->kernel = kernel;
   if (options.barnesHut) throw std::invalid_argument("unsupported on the GPU path: Barnes-Hut plans (SURVEY §8f 'next')");
@@ -324,6 +354,25 @@ void destroyPlan(DevicePlan* plan) {
   if (side) cudaStreamDestroy(side);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+}
+
+long long kernelLaunches(const DevicePlan& plan, int nrhs) {
+  auto chunks = [&](int perRhsDoubles) {
+    const size_t perRhs = static_cast<size_t>(128) * perRhsDoubles * sizeof(double);
+    const int chunk = std::max(1, static_cast<int>((200 * 1024) / perRhs));
+    return (nrhs + chunk - 1) / chunk;
+  };
+  long long k = 2;  // gather_y, scatter_z
+  if (plan.useMoments) {
+    if (!plan.p2mTilesHost.empty()) k += chunks(plan.monoCount);  // p2m
+    for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
+    k += !plan.farNodesHost.empty();  // to_coef
+  } else if (!plan.s2mTilesHost.empty()) {
+    k += chunks(plan.P);
+  }
+  k += plan.nearSym ? !plan.blockTilesHost.empty() : !plan.nearTilesHost.empty();
+  k += !plan.farTilesHost.empty();
+  return k;
 }
 
 void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t st) {

@@ -157,6 +157,12 @@ struct DevicePlan {
   std::vector<FktbBlockTile> blockTilesHost;
   DeviceBuffer<FktbBlockTile> dBlockTiles;
   long long symPairs = 0, oneWayPairs = 0;
+  // Target shard (shard.cu): owned tree positions [shardLo, shardHi) and the
+  // owned sub-range [sub[2b], sub[2b+1]) of every node's far / near list
+  // (empty = whole lists).
+  int shard = 0, shards = 1;
+  uint32_t shardLo = 0, shardHi = 0;
+  std::vector<long long> farSub, nearSub;
   // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
   // on repeat calls (launch-bound small problems). Cleared on reallocation.
   std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
@@ -173,6 +179,18 @@ void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cuda
 const double* expTableDevice();
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
+// Multi-GPU target sharding (shard.cu).
+void setShard(DevicePlan& plan, int shard, int shards);
+std::vector<uint32_t> shardCuts(const DeviceTree& t, int P, int shards);
+std::vector<uint32_t> shardCutsFromLeaves(const std::vector<std::pair<uint32_t, unsigned long long>>& leafEnd, int shards,
+                                          uint32_t n);
+unsigned long long farPairWeight(int P);
+void rebuildTiles(DevicePlan& plan);
+// Grow the per-nrhs workspaces (moments, permuted y/z); clears captured graphs.
+void ensureWorkspace(DevicePlan& plan, int nrhs);
+// Number of this library's kernels one multiply launches (memsets excluded).
+long long kernelLaunches(const DevicePlan& plan, int nrhs);
+
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void buildNearBlocks(DevicePlan& plan, bool oneWayOnly = false);
 bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
