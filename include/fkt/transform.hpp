@@ -47,7 +47,7 @@ struct FktOptions {
   int leafCapacity = 512;
   CompressionMode compression = CompressionMode::Auto;
   bool eagerOperators = true;  // accepted; the GPU recomputes operators in registers
-  bool barnesHut = false;      // not offered on the GPU path
+  bool barnesHut = false;      // monopole far field about centres of mass (csrc/bh.cu); forces p = 0
   int threads = 0;             // CPU knob of the reference, ignored
   std::optional<double> diagonal;
   int nearPrecision = 64;      // additive: 32 selects the FP32 fast near field

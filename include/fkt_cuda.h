@@ -43,7 +43,7 @@ typedef struct fkt_options {
   int leaf_capacity;
   int compression;
   int eager_operators; /* accepted; the GPU always recomputes operators in registers */
-  int barnes_hut;      /* not offered on the GPU path (FKT_ERR_UNSUPPORTED) */
+  int barnes_hut;      /* Barnes-Hut monopole far field (transform.cpp:44-60,131-146); forces p = 0 */
   int threads;         /* CPU-only knob, ignored */
   int has_diagonal;
   double diagonal;

@@ -95,8 +95,10 @@ class RefPlan:
     """The reference fkt::FktPlan (transform.cpp:39-204), CPU."""
 
     def __init__(self, x, kernel: str, params=None, p=4, theta=0.75, leaf=512, compression=0, eager=False,
-                 threads=0, diagonal=None):
+                 threads=0, diagonal=None, barnes_hut=False):
         L = lib()
+        if barnes_hut:
+            compression = -1  # ref_driver.cpp: FktOptions::barnesHut
         self.x = np.ascontiguousarray(x, dtype=np.float64)
         self.n, self.d = self.x.shape
         self.h = L.fktref_plan_create(self.n, self.d, _dp(self.x), kernel.encode(), _kv(params), p, theta, leaf,

@@ -154,6 +154,8 @@ void* fktref_plan_create(int n, int d, const double* x, const char* kernel, cons
     o.p = p;
     o.theta = theta;
     o.leafCapacity = leaf;
+    // compression -1: a Barnes-Hut plan (FktOptions::barnesHut, transform.cpp:44-60)
+    o.barnesHut = compression == -1;
     o.compression = compression == 1 ? fkt::CompressionMode::On
                     : compression == 2 ? fkt::CompressionMode::Off
                                        : fkt::CompressionMode::Auto;

@@ -355,6 +355,10 @@ class FktPlan:
         options = options or FktOptions()
         self._cloud = PointCloud(cloud.n, cloud.d, cloud.x.copy())
         self._kernel = kernel
+        if options.barnesHut:  # transform.cpp:44: a Barnes-Hut plan has p = 0
+            import dataclasses
+
+            options = dataclasses.replace(options, p=0)
         self._options = options
         self.d = cloud.d
         h = C.c_void_p()
@@ -474,6 +478,15 @@ class FktPlan:
 def plan(cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None) -> FktPlan:
     """fkt::plan (transform.cpp:206-208)."""
     return FktPlan(cloud, kernel, options)
+
+
+def barnesHutMultiply(plan: FktPlan, y) -> np.ndarray:
+    """fkt::barnesHutMultiply (transform.cpp:239-243): multiply on a plan built
+    with FktOptions(barnesHut=True) (monopole far field about the centres of
+    mass, csrc/bh.cu)."""
+    if not plan.options().barnesHut:
+        raise InvalidArgument("barnesHutMultiply requires a plan built with the Barnes-Hut option")
+    return plan.multiply(y)
 
 
 def denseMultiply(cloud: PointCloud, kernel: IsotropicKernel, y, diagonal: Optional[float] = None,

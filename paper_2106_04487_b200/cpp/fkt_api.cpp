@@ -245,6 +245,7 @@ FktPlan::FktPlan(PointCloud cloud, KernelPtr kernel, const FktOptions& options)
   fkt_plan_t h = nullptr;
   check(fkt_plan_create(cloud_.n, cloud_.d, cloud_.x.data(), kernel_->name().c_str(), pa.k(), pa.v(), pa.n(), &o, &h));
   h_ = h;
+  if (options_.barnesHut) options_.p = 0;  // transform.cpp:44
 }
 
 FktPlan::~FktPlan() {

@@ -292,22 +292,26 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   plan->shardHi = static_cast<uint32_t>(n);
   plan->options = options;
   plan->kernel = kernel;
-  if (options.barnesHut) throw std::invalid_argument("unsupported on the GPU path: Barnes-Hut plans (SURVEY §8f 'next')");
+  if (options.barnesHut) plan->options.p = 0;  // transform.cpp:44
   // Validation order follows the reference constructor (transform.cpp:39-80).
   if (options.leafCapacity < 1) throw std::invalid_argument("leaf capacity must be >= 1");
   if (n < 1) throw std::invalid_argument("point cloud must be nonempty");
-  if (options.p < 0) throw std::invalid_argument("plan requires p >= 0");
+  if (plan->options.p < 0) throw std::invalid_argument("plan requires p >= 0");
   if (!(options.theta > 0.0 && options.theta < 1.0)) throw std::invalid_argument("theta must be in (0, 1)");
-  if (d < 2) throw std::invalid_argument("HarmonicBasis requires d >= 2");
-  const CoefTable& table = coefTable(d, options.p);  // OrderTooLarge for p > 20
+  // Barnes-Hut plans return before the expansion tables (transform.cpp:48-59):
+  // no coefficient table, harmonic basis (so any d >= 1) or compression.
+  const bool bh = options.barnesHut;
+  if (!bh && d < 2) throw std::invalid_argument("HarmonicBasis requires d >= 2");
+  const CoefTable* table = bh ? nullptr : &coefTable(d, plan->options.p);  // OrderTooLarge for p > 20
   bool compress = false;
-  if (options.compression == 0)
+  if (bh) {
+  } else if (options.compression == 0)
     compress = kernel.recurrence.has_value();
   else if (options.compression == 1) {
     if (!kernel.recurrence) throw NotRecurrenceKernelError(kernel.name);
     compress = true;
   }
-  if (!specialised(d, options.p) && (d - 2) * (options.p + 1) * (options.p + 2) / 2 > genericGMax())
+  if (!bh && !specialised(d, options.p) && (d - 2) * (options.p + 1) * (options.p + 2) / 2 > genericGMax())
     throw std::invalid_argument("unsupported on the GPU path: (d, p) too large for the runtime far-field kernels");
 
   FKTB_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
@@ -318,12 +322,24 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
   computeSetsGpu(*plan->tree, options.theta);
 
-  plan->harmonics = std::make_unique<HarmonicStructure>(d, options.p);
-  if (compress) plan->factors = radialCompression(kernel, table, options.p);
   plan->compressed = compress;
-  buildFarParams(*plan);
+  if (bh) {
+    // one coefficient per node: the source total (coefficientCount() == 1, transform.cpp:95)
+    auto fp = std::make_unique<FktbFarParams>();
+    std::memset(fp.get(), 0, sizeof(FktbFarParams));
+    fp->d = d;
+    fp->P = fp->Pref = fp->H = 1;
+    plan->far = std::move(fp);
+    plan->P = plan->H = 1;
+  } else {
+    plan->harmonics = std::make_unique<HarmonicStructure>(d, plan->options.p);
+    if (compress) plan->factors = radialCompression(kernel, *table, plan->options.p);
+    buildFarParams(*plan);
+  }
   buildTiles(*plan);
-  {
+  if (bh) {
+    buildBarnesHut(*plan);
+  } else {
     const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
     // "1" enables the symmetric leaf-pair near field (nearsym.cu). Measured
@@ -368,7 +384,7 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
     for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
     k += !plan.farNodesHost.empty();  // to_coef
   } else if (!plan.s2mTilesHost.empty()) {
-    k += chunks(plan.P);
+    k += plan.options.barnesHut ? 1 : chunks(plan.P);
   }
   k += plan.nearSym ? !plan.blockTilesHost.empty() : !plan.nearTilesHost.empty();
   k += !plan.farTilesHost.empty();
@@ -376,7 +392,9 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
 }
 
 void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t st) {
-  if (plan.useMoments)
+  if (plan.options.barnesHut)
+    launchBHSums(plan, yp, moments, nrhs, st);
+  else if (plan.useMoments)
     launchS2MMoments(plan, yp, moments, nrhs, st);
   else
     launchS2M(plan, yp, moments, nrhs, st);

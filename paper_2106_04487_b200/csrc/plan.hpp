@@ -163,6 +163,8 @@ struct DevicePlan {
   int shard = 0, shards = 1;
   uint32_t shardLo = 0, shardHi = 0;
   std::vector<long long> farSub, nearSub;
+  // Barnes-Hut plans (bh.cu): per-node centres of mass, nodes x d.
+  DeviceBuffer<double> dCom;
   // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
   // on repeat calls (launch-bound small problems). Cleared on reallocation.
   std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
@@ -190,6 +192,11 @@ void rebuildTiles(DevicePlan& plan);
 void ensureWorkspace(DevicePlan& plan, int nrhs);
 // Number of this library's kernels one multiply launches (memsets excluded).
 long long kernelLaunches(const DevicePlan& plan, int nrhs);
+
+// Barnes-Hut monopole far field (bh.cu).
+void buildBarnesHut(DevicePlan& plan);
+void launchBHSums(const DevicePlan& plan, const double* yp, double* totals, int nrhs, cudaStream_t stream);
+void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int nrhs, cudaStream_t stream);
 
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void buildNearBlocks(DevicePlan& plan, bool oneWayOnly = false);

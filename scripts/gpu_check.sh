@@ -1,1 +1,1 @@
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --sharded --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/sharded.log 2>&1; tail -3 gpurun_out/sharded.log
+timeout 1200 python -m pytest tests/test_gpu_barnes_hut.py tests/test_gpu_distributed.py tests/test_gpu_reference_suite.py -q -x 2>&1 | tail -15

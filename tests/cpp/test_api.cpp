@@ -194,6 +194,32 @@ static void device_multiply_and_multi_rhs() {
   }
 }
 
+static void barnes_hut_baseline() {  // test_transform.cpp:188-222
+  Rng rng(909);
+  auto k = makeKernel("cauchy");
+  const int n = 3000;
+  PointCloud cloud = cubeCloud(n, 2, rng);
+  const auto y = normalVector(n, rng);
+  const auto exact = denseMultiply(cloud, *k, y);
+  FktOptions bh;
+  bh.barnesHut = true;
+  bh.leafCapacity = 128;
+  FktPlan bhPlan = plan(cloud, k, bh);
+  CHECK(bhPlan.options().p == 0 && bhPlan.coefficientCount() == 1);
+  std::vector<double> zero(n, 0.0);
+  for (double v : barnesHutMultiply(bhPlan, zero)) CHECK(v == 0.0);
+  const auto z1 = barnesHutMultiply(bhPlan, y);
+  const auto z2 = barnesHutMultiply(bhPlan, y);
+  CHECK(relativeError(z1, z2) <= 1e-15);  // FP64 atomics: roundoff-equal, not bitwise
+  FktOptions fkt2;
+  fkt2.p = 2;
+  fkt2.leafCapacity = 128;
+  const double bhErr = relativeError(z1, exact);
+  CHECK(relativeError(plan(cloud, k, fkt2).multiply(y), exact) < bhErr);
+  FktPlan plain = plan(cloud, k, fkt2);
+  CHECK_THROWS_AS(barnesHutMultiply(plain, y), std::invalid_argument);
+}
+
 int main() {
   dense_basics();
   single_leaf_exact();
@@ -203,6 +229,7 @@ int main() {
   coefficient_count_and_errors();
   tree_structure();
   device_multiply_and_multi_rhs();
+  barnes_hut_baseline();
   std::printf("cpp api: %d failures\n", g_fail);
   return g_fail;
 }

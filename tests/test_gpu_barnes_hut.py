@@ -1,0 +1,59 @@
+"""GPU: Barnes-Hut plans (FktOptions.barnesHut, csrc/bh.cu) -- the reference's
+monopole baseline (transform.cpp:44-60, 131-146, 239-243).
+
+Ports test_transform.cpp:188-222 ("barnes-hut baseline") and checks parity
+with the reference's own Barnes-Hut multiply (oracle/_ref) on the same inputs.
+One deliberate difference: the reference's repeated runs are bit-identical
+(a fixed thread merge order); the GPU accumulates z with FP64 atomics, so
+repeated runs agree to roundoff (asserted at 1e-15 relative)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(fkt, x, name="cauchy", prm=None, **opt):
+    return fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(name, prm or {}), fkt.FktOptions(barnesHut=True, **opt))
+
+
+def test_reference_barnes_hut_baseline(fkt, ref):  # test_transform.cpp:188-222
+    x, y = fkt.synthCloud("cube", 3000, 2, 909)
+    bh = _plan(fkt, x, leafCapacity=128)
+    assert bh.options().p == 0 and bh.coefficientCount() == 1 and not bh.compressed()
+    assert np.all(fkt.barnesHutMultiply(bh, np.zeros(3000)) == 0.0)
+    z1 = fkt.barnesHutMultiply(bh, y)
+    z2 = fkt.barnesHutMultiply(bh, y)
+    assert np.linalg.norm(z1 - z2) / np.linalg.norm(z1) <= 1e-15
+    # "single point per node is exact" (:206-214): with leafCapacity 1 the
+    # INTERNAL nodes still have far sets, so the monopole is not exact; the
+    # reference itself gives ~7e-2 here (it misses its own 1e-12 bound). The
+    # port asserts parity with the reference's result instead.
+    xt, yt = fkt.synthCloud("cube", 40, 2, 910)
+    tiny = _plan(fkt, xt, leafCapacity=1)
+    zt = fkt.barnesHutMultiply(tiny, yt)
+    zr = ref.RefPlan(xt, "cauchy", {}, p=0, theta=0.75, leaf=1, barnes_hut=True).multiply(yt)
+    assert fkt.relativeError(zt, zr) <= 1e-13
+    # a p = 2 transform beats the monopole baseline at equal theta
+    exact = fkt.denseMultiply(fkt.PointCloud.from_array(x), fkt.makeKernel("cauchy"), y)
+    f2 = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel("cauchy"), fkt.FktOptions(p=2, leafCapacity=128))
+    assert fkt.relativeError(f2.multiply(y), exact) < fkt.relativeError(z1, exact)
+
+
+CASES = [("cube", 20000, 2, "cauchy", {"sigma": 1.0}, 128, 0.75, None),
+         ("cube", 50000, 3, "matern32", {"sigma": 1.0, "rho": 0.1}, 256, 0.5, None),
+         ("sphere", 40000, 3, "inverse-r", {}, 256, 0.5, None),
+         ("sphere", 40000, 3, "inverse-r", {}, 256, 0.5, 3.0),
+         ("mixture", 30000, 5, "gaussian", {}, 512, 0.75, None),
+         ("cube", 8000, 1, "exponential", {}, 64, 0.5, None)]  # d = 1: no harmonic basis needed
+
+
+@pytest.mark.parametrize("kind,n,d,name,prm,leaf,theta,diag", CASES)
+def test_barnes_hut_matches_reference(fkt, ref, kind, n, d, name, prm, leaf, theta, diag):
+    x, y = fkt.synthCloud(kind, n, d, 31)
+    kw = {} if diag is None else {"diagonal": diag}
+    pl = _plan(fkt, x, name, prm, leafCapacity=leaf, theta=theta, **kw)
+    rp = ref.RefPlan(x, name, prm, p=0, theta=theta, leaf=leaf, barnes_hut=True, diagonal=diag)
+    zr = rp.multiply(y)
+    assert fkt.relativeError(fkt.barnesHutMultiply(pl, y), zr) <= 1e-12
+    W = np.stack([y, -y, np.roll(y, 11)], axis=1)
+    assert np.linalg.norm(pl.multiply(W) - rp.multiply(W)) / np.linalg.norm(rp.multiply(W)) <= 1e-12

@@ -73,6 +73,18 @@ def test_sharded_sum_equals_unsharded(fkt, kind, n, d, name, prm, p, leaf, theta
     assert np.linalg.norm(pl.multiply_device(yd).cpu().numpy() - z1) / np.linalg.norm(z1) <= 1e-14
 
 
+def test_sharded_barnes_hut(fkt):
+    import torch
+
+    x, y = fkt.synthCloud("sphere", 100000, 3, 8)
+    pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel("inverse-r"),
+                  fkt.FktOptions(theta=0.5, leafCapacity=256, barnesHut=True))
+    yd = torch.from_numpy(y).cuda()
+    z1 = pl.multiply_device(yd).cpu().numpy()
+    z, _ = _simulate(fkt, pl, yd, 3)
+    assert np.linalg.norm(z.cpu().numpy() - z1) / np.linalg.norm(z1) <= 1e-13
+
+
 def test_sharded_multi_rhs(fkt):
     import torch
 

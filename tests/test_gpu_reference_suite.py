@@ -214,8 +214,8 @@ def test_plan_errors(fkt):
         fkt.plan(P(fkt, x), k, fkt.FktOptions(leafCapacity=0))
     with pytest.raises(fkt.NotRecurrenceKernelError):
         fkt.plan(P(fkt, x), fkt.makeKernel("matern32"), fkt.FktOptions(compression=fkt.CompressionMode.On))
-    with pytest.raises(fkt.UnsupportedOnGpuError):
-        fkt.plan(P(fkt, x), k, fkt.FktOptions(barnesHut=True))
+    with pytest.raises(fkt.InvalidArgument):  # barnesHutMultiply on a plain plan (transform.cpp:240-241)
+        fkt.barnesHutMultiply(p, np.zeros(100))
     with pytest.raises(fkt.DimensionMismatchError):
         fkt.denseMultiply(P(fkt, x), k, np.zeros(3))
 
