@@ -122,6 +122,48 @@ long long fkt_plan_kernel_launches(fkt_plan_t plan, int nrhs);
 int fkt_shard_cuts(const uint32_t* leaf_end, const unsigned long long* leaf_cum_cost, int leaves, int shards, uint32_t n,
                    uint32_t* cuts);
 
+/* Gaussian-process solves (reference proj/include/fkt/gp.hpp, gp.cpp). The
+ * CG iterates stay in HBM (x, r, z, p, Ap); each iteration is one device MVM
+ * plus small vector kernels, the host reads two scalars per iteration. */
+typedef struct fkt_cg_diagnostics { /* CgDiagnostics, gp.hpp:35-40 */
+  int iterations;
+  double final_residual; /* relative to |b| */
+  int converged;
+  int restarts;
+} fkt_cg_diagnostics;
+
+/* cgSolve(NoisyOperator(plan, noise), rhs, ...) — gp.cpp:20-26, 58-124.
+ * Host buffers of length n. restart_on_increase = 1 is the reference's rule
+ * (restart from the current iterate whenever |r| grows, gp.cpp:100-111);
+ * 0 (additive) runs textbook CG. */
+int fkt_cg_solve(fkt_plan_t plan, const double* noise, const double* rhs, double tolerance, int max_iterations,
+                 int jacobi, int restart_on_increase, double* x, fkt_cg_diagnostics* diag);
+/* The same over the dense operator NoisyOperator(cloud, kernel, noise,
+ * diagonal) — gp.cpp:28-37 (K7 rows on the GPU). */
+int fkt_cg_solve_dense(int n, int d, const double* points, const char* kernel, const char* const* keys,
+                       const double* values, int nparams, int has_diagonal, double diagonal, const double* noise,
+                       const double* rhs, double tolerance, int max_iterations, int jacobi, int restart_on_increase,
+                       double* x, fkt_cg_diagnostics* diag);
+
+typedef struct fkt_gp_options { /* GpOptions, gp.hpp:51-58 */
+  fkt_options fkt;
+  double cg_tolerance;
+  int cg_max_iterations;
+  int jacobi;
+  int dense;
+  int has_prior_mean;
+  double prior_mean;
+  int restart_on_increase; /* additive; 1 = the reference's CG restart rule (default) */
+} fkt_gp_options;
+void fkt_default_gp_options(fkt_gp_options* opt);
+
+/* gpPosteriorMean(train, y, noise, kernel, test, options) — gp.cpp:126-177:
+ * CG on the train plan, then one multiply on the concatenated train+test
+ * cloud with the solution zero-padded on the test block. mean: n_test. */
+int fkt_gp_posterior_mean(int n_train, int d, const double* train_x, const double* y, const double* noise,
+                          const char* kernel, const char* const* keys, const double* values, int nparams, int n_test,
+                          const double* test_x, const fkt_gp_options* opt, double* mean, fkt_cg_diagnostics* diag);
+
 /* Tree view of a plan (borrowed; valid while the plan lives). */
 fkt_tree_t fkt_plan_tree(fkt_plan_t plan);
 

@@ -54,6 +54,12 @@ def lib():
             "fktref_addition_normalizer": (C.c_double, C.c_int, C.c_int),
             "fktref_harmonics": (C.c_int, C.c_int, C.c_int, d, d),
             "fktref_kernel_jet": (C.c_int, C.c_char_p, C.c_char_p, C.c_double, C.c_int, d),
+            "fktref_cg_solve": (C.c_int, C.c_int, C.c_int, d, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double,
+                                C.c_int, C.c_int, C.c_double, d, d, C.c_double, C.c_int, C.c_int, d, i32, d, i32,
+                                i32),
+            "fktref_gp_posterior_mean": (C.c_int, C.c_int, C.c_int, d, d, d, C.c_char_p, C.c_char_p, C.c_int, d,
+                                         C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                         C.c_int, C.c_int, C.c_int, C.c_double, d, i32, d, i32, i32),
         }
         for name, (res, *args) in sigs.items():
             f = getattr(L, name)
@@ -233,3 +239,44 @@ def fingerprint_arrays(order, far_off, far, near_off, near, radius, center):
         for c in cb[b].tolist():
             g = ((g ^ c) * P) & M
     return f"{ho:016x}", f"{h:016x}", f"{g:016x}"
+
+
+def _diag(it, res, conv, rs):
+    return {"iterations": it.value, "finalResidual": res.value, "converged": bool(conv.value), "restarts": rs.value}
+
+
+def cg_solve(x, kernel, params, noise, rhs, tol, maxit, jacobi=False, plan=None, diagonal=None):
+    """The reference cgSolve (gp.cpp:58-124). plan=None: dense NoisyOperator;
+    plan=dict(p=, theta=, leaf=): NoisyOperator over a reference FktPlan.
+    kernel "zero" is test_gp.cpp's zero kernel."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n, d = x.shape
+    noise = np.ascontiguousarray(noise, dtype=np.float64)
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    out = np.empty(n)
+    it, res, conv, rs = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+    pl = plan or {}
+    if lib().fktref_cg_solve(n, d, _dp(x), kernel.encode(), _kv(params), int(plan is not None), int(pl.get("p", 4)),
+                             float(pl.get("theta", 0.75)), int(pl.get("leaf", 512)), int(diagonal is not None),
+                             float(diagonal or 0.0), _dp(noise), _dp(rhs), float(tol), int(maxit), int(jacobi),
+                             _dp(out), C.byref(it), C.byref(res), C.byref(conv), C.byref(rs)) != 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return out, _diag(it, res, conv, rs)
+
+
+def gp_posterior_mean(train, y, noise, kernel, params, test, p=4, theta=0.75, leaf=512, diagonal=None, tol=1e-10,
+                      maxit=1000, jacobi=False, dense=False, prior=None):
+    """The reference gpPosteriorMean (gp.cpp:126-177)."""
+    train = np.ascontiguousarray(train, dtype=np.float64)
+    test = np.ascontiguousarray(test, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    noise = np.ascontiguousarray(noise, dtype=np.float64)
+    mean = np.empty(test.shape[0])
+    it, res, conv, rs = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+    if lib().fktref_gp_posterior_mean(train.shape[0], train.shape[1], _dp(train), _dp(y), _dp(noise),
+                                      kernel.encode(), _kv(params), test.shape[0], _dp(test), int(p), float(theta),
+                                      int(leaf), int(diagonal is not None), float(diagonal or 0.0), float(tol),
+                                      int(maxit), int(jacobi), int(dense), int(prior is not None), float(prior or 0.0),
+                                      _dp(mean), C.byref(it), C.byref(res), C.byref(conv), C.byref(rs)) != 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    return mean, _diag(it, res, conv, rs)

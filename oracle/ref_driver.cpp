@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "fkt/gp.hpp"
 #include "fkt/harmonics.hpp"
 #include "fkt/synthetic.hpp"
 #include "fkt/transform.hpp"
@@ -260,6 +261,91 @@ int fktref_dense(int n, int d, const double* x, const char* kernel, const char* 
     if (hasDiag) dg = diag;
     auto out = fkt::denseMultiply(cloud, *k, std::span<const double>(y, static_cast<std::size_t>(n)), dg, threads);
     std::memcpy(z, out.data(), out.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// --- reference GP / CG (gp.cpp) ---------------------------------------------
+namespace {
+// test_gp.cpp:14-18: the zero kernel (a user lambda the GPU path cannot run)
+fkt::KernelPtr refKernel(const char* name, const char* params) {
+  if (std::string(name) == "zero")
+    return std::make_shared<fkt::IsotropicKernel>(
+        "zero", fkt::IsotropicKernel::Params{}, [](double) { return 0.0; },
+        [](const fkt::Jet& r) { return fkt::Jet::constant(0.0, r.center(), r.order()); }, std::nullopt, 0.0);
+  return fkt::makeKernel(name, parseParams(params));
+}
+void putDiag(const fkt::CgDiagnostics& dg, int* it, double* res, int* conv, int* rs) {
+  *it = dg.iterations;
+  *res = dg.finalResidual;
+  *conv = dg.converged ? 1 : 0;
+  *rs = dg.restarts;
+}
+}  // namespace
+
+// cgSolve (gp.cpp:58-124) over NoisyOperator(plan, noise) when usePlan, else
+// the dense NoisyOperator(cloud, kernel, noise, diagonal).
+int fktref_cg_solve(int n, int d, const double* x, const char* kernel, const char* params, int usePlan, int p,
+                    double theta, int leaf, int hasDiag, double diag, const double* noise, const double* rhs,
+                    double tol, int maxit, int jacobi, double* out, int* it, double* res, int* conv, int* rs) {
+  try {
+    fkt::PointCloud cloud(n, d);
+    std::memcpy(cloud.x.data(), x, static_cast<std::size_t>(n) * d * sizeof(double));
+    auto k = refKernel(kernel, params);
+    std::optional<double> dg;
+    if (hasDiag) dg = diag;
+    std::vector<double> nz(noise, noise + n);
+    std::unique_ptr<fkt::FktPlan> plan;
+    std::unique_ptr<fkt::NoisyOperator> op;
+    if (usePlan) {
+      fkt::FktOptions o;
+      o.p = p;
+      o.theta = theta;
+      o.leafCapacity = leaf;
+      o.diagonal = dg;
+      plan = std::make_unique<fkt::FktPlan>(cloud, k, o);
+      op = std::make_unique<fkt::NoisyOperator>(*plan, nz);
+    } else {
+      op = std::make_unique<fkt::NoisyOperator>(cloud, k, nz, dg);
+    }
+    const auto r = fkt::cgSolve(*op, std::span<const double>(rhs, static_cast<std::size_t>(n)), tol, maxit, jacobi != 0);
+    std::memcpy(out, r.x.data(), r.x.size() * sizeof(double));
+    putDiag(r.diagnostics, it, res, conv, rs);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// gpPosteriorMean (gp.cpp:126-177).
+int fktref_gp_posterior_mean(int nTrain, int d, const double* trainX, const double* y, const double* noise,
+                             const char* kernel, const char* params, int nTest, const double* testX, int p,
+                             double theta, int leaf, int hasDiag, double diag, double tol, int maxit, int jacobi,
+                             int dense, int hasPrior, double prior, double* mean, int* it, double* res, int* conv,
+                             int* rs) {
+  try {
+    fkt::PointCloud train(nTrain, d), test(nTest, d);
+    std::memcpy(train.x.data(), trainX, static_cast<std::size_t>(nTrain) * d * sizeof(double));
+    if (nTest > 0) std::memcpy(test.x.data(), testX, static_cast<std::size_t>(nTest) * d * sizeof(double));
+    fkt::GpOptions o;
+    o.fkt.p = p;
+    o.fkt.theta = theta;
+    o.fkt.leafCapacity = leaf;
+    if (hasDiag) o.fkt.diagonal = diag;
+    o.cgTolerance = tol;
+    o.cgMaxIterations = maxit;
+    o.jacobiPreconditioner = jacobi != 0;
+    o.dense = dense != 0;
+    if (hasPrior) o.priorMean = prior;
+    const auto pr = fkt::gpPosteriorMean(train, std::span<const double>(y, static_cast<std::size_t>(nTrain)),
+                                         std::span<const double>(noise, static_cast<std::size_t>(nTrain)),
+                                         refKernel(kernel, params), test, o);
+    std::memcpy(mean, pr.mean.data(), pr.mean.size() * sizeof(double));
+    putDiag(pr.diagnostics, it, res, conv, rs);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -526,6 +526,139 @@ def relativeError(approx, exact) -> float:
     return out.value
 
 
+# --- Gaussian processes (reference proj/include/fkt/gp.hpp, gp.cpp) -------------
+@dataclass
+class CgDiagnostics:
+    """fkt::CgDiagnostics (gp.hpp:35-40)."""
+
+    iterations: int = 0
+    finalResidual: float = 0.0
+    converged: bool = False
+    restarts: int = 0
+
+    @staticmethod
+    def _from(c) -> "CgDiagnostics":
+        return CgDiagnostics(int(c.iterations), float(c.final_residual), bool(c.converged), int(c.restarts))
+
+
+@dataclass
+class CgResult:
+    """fkt::CgResult (gp.hpp:42-45)."""
+
+    x: np.ndarray
+    diagnostics: CgDiagnostics
+
+
+class NoisyOperator:
+    """fkt::NoisyOperator (gp.hpp:17-33, gp.cpp:20-44): y -> K y + noise .* y.
+
+    NoisyOperator(plan, noise) uses the FKT plan; NoisyOperator(cloud, kernel,
+    noise, diagonal=None) the dense product (on the GPU)."""
+
+    def __init__(self, a, b, c=None, diagonal: Optional[float] = None):
+        if isinstance(a, FktPlan):
+            self._plan, self._cloud, self._kernel, self._diag = a, a.cloud(), a.kernel(), a.options().diagonal
+            noise = b
+        else:
+            self._plan, self._cloud, self._kernel, self._diag = None, a, b, diagonal
+            noise = c
+        self._noise = _f64(noise).ravel()
+        if self._noise.size != self._cloud.n:
+            raise DimensionMismatchError("NoisyOperator: noise length does not match the point count")
+        # gp.cpp:10-16: K(0) under the diagonal convention, 0 when singular
+        v0 = self._kernel.valueAtZero()
+        self._k0 = float(self._diag) if self._diag is not None else (float(v0) if v0 is not None else 0.0)
+
+    def size(self) -> int:
+        return self._cloud.n
+
+    def noise(self) -> np.ndarray:
+        return self._noise
+
+    def kernelDiagonal(self) -> float:
+        return self._k0
+
+    def apply(self, y) -> np.ndarray:
+        y = _f64(y).ravel()
+        if y.size != self._cloud.n:
+            raise DimensionMismatchError("NoisyOperator: vector length mismatch")
+        z = self._plan.multiply(y) if self._plan is not None else denseMultiply(self._cloud, self._kernel, y,
+                                                                                    self._diag)
+        return z + self._noise * y
+
+
+def cgSolve(op: NoisyOperator, rhs, tolerance: float, maxIterations: int,
+            jacobiPreconditioner: bool = False, restartOnIncrease: bool = True) -> CgResult:
+    """fkt::cgSolve (gp.cpp:58-124); the iterates live on the GPU (csrc/gp.cu).
+
+    restartOnIncrease (additive, default = the reference): restart from the
+    current iterate whenever the residual norm grows (gp.cpp:100-111). CG
+    residuals are not monotone, so on smooth kernels the rule fires about every
+    other iteration and the solve stalls -- exactly as in the reference;
+    False runs textbook CG."""
+    b = _f64(rhs).ravel()
+    if b.size != op.size():
+        raise DimensionMismatchError("cgSolve: rhs length mismatch")
+    if not tolerance > 0.0:
+        raise InvalidArgument("cgSolve requires a positive tolerance")
+    x = np.empty(b.size)
+    dg = _L.FktCgDiagnosticsC()
+    if op._plan is not None:
+        _check(lib.fkt_cg_solve(op._plan._h, _dptr(op._noise), _dptr(b), float(tolerance), int(maxIterations),
+                                int(bool(jacobiPreconditioner)), int(bool(restartOnIncrease)), _dptr(x), C.byref(dg)))
+    else:
+        k, v, n = _params(op._kernel.parameters())
+        cl = op._cloud
+        _check(lib.fkt_cg_solve_dense(cl.n, cl.d, _dptr(cl.x), op._kernel.name().encode(), k, v, n,
+                                      int(op._diag is not None), float(op._diag or 0.0), _dptr(op._noise), _dptr(b),
+                                      float(tolerance), int(maxIterations), int(bool(jacobiPreconditioner)),
+                                      int(bool(restartOnIncrease)), _dptr(x), C.byref(dg)))
+    return CgResult(x, CgDiagnostics._from(dg))
+
+
+@dataclass
+class GpOptions:
+    """fkt::GpOptions (gp.hpp:51-58)."""
+
+    fkt: FktOptions = field(default_factory=FktOptions)
+    cgTolerance: float = 1e-10
+    cgMaxIterations: int = 1000
+    jacobiPreconditioner: bool = False
+    dense: bool = False
+    priorMean: Optional[float] = None
+    restartOnIncrease: bool = True  # additive; see cgSolve
+
+
+@dataclass
+class GpPrediction:
+    """fkt::GpPrediction (gp.hpp:60-63)."""
+
+    mean: np.ndarray
+    diagnostics: CgDiagnostics
+
+
+def gpPosteriorMean(train: PointCloud, y, noise, kernel: IsotropicKernel, test: PointCloud,
+                    options: Optional[GpOptions] = None) -> GpPrediction:
+    """fkt::gpPosteriorMean (gp.cpp:126-177) on the GPU."""
+    o = options or GpOptions()
+    y, noise = _f64(y).ravel(), _f64(noise).ravel()
+    if y.size != train.n or noise.size != train.n:
+        raise DimensionMismatchError("gpPosteriorMean: training vector lengths must match the cloud")
+    if test.d != train.d:
+        raise DimensionMismatchError("gpPosteriorMean: train/test dimension mismatch")
+    oc = _L.FktGpOptionsC(o.fkt._c(), float(o.cgTolerance), int(o.cgMaxIterations), int(bool(o.jacobiPreconditioner)),
+                          int(bool(o.dense)), int(o.priorMean is not None), float(o.priorMean or 0.0),
+                          int(bool(o.restartOnIncrease)))
+    mean = np.empty(test.n)
+    dg = _L.FktCgDiagnosticsC()
+    k, v, n = _params(kernel.parameters())
+    tx = _f64(test.x) if test.n > 0 else np.zeros((1, train.d))
+    _check(lib.fkt_gp_posterior_mean(train.n, train.d, _dptr(_f64(train.x)), _dptr(y), _dptr(noise),
+                                     kernel.name().encode(), k, v, n, test.n, _dptr(tx), C.byref(oc),
+                                     _dptr(mean) if test.n > 0 else None, C.byref(dg)))
+    return GpPrediction(mean, CgDiagnostics._from(dg))
+
+
 def expansionSize(d: int, p: int) -> int:
     r = lib.fkt_expansion_size(int(d), int(p))
     if r < 0:

@@ -42,6 +42,17 @@ class FktOptionsC(C.Structure):
     ]
 
 
+class FktCgDiagnosticsC(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("final_residual", C.c_double), ("converged", C.c_int),
+                ("restarts", C.c_int)]
+
+
+class FktGpOptionsC(C.Structure):
+    _fields_ = [("fkt", FktOptionsC), ("cg_tolerance", C.c_double), ("cg_max_iterations", C.c_int),
+                ("jacobi", C.c_int), ("dense", C.c_int), ("has_prior_mean", C.c_int), ("prior_mean", C.c_double),
+                ("restart_on_increase", C.c_int)]
+
+
 class FktPlanInfoC(C.Structure):
     _fields_ = [
         ("n", C.c_int),
@@ -89,6 +100,13 @@ SIGNATURES = {
     "fkt_plan_set_shard": (C.c_int, C.c_void_p, C.c_int, C.c_int),
     "fkt_plan_shard_range": (C.c_int, C.c_void_p, _ll, _ll),
     "fkt_plan_moments_device": (C.c_int, C.c_void_p, C.POINTER(C.POINTER(C.c_double)), _ll),
+    "fkt_default_gp_options": (None, C.POINTER(FktGpOptionsC)),
+    "fkt_cg_solve": (C.c_int, C.c_void_p, _d, _d, C.c_double, C.c_int, C.c_int, C.c_int, _d,
+                     C.POINTER(FktCgDiagnosticsC)),
+    "fkt_cg_solve_dense": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int, C.c_int, C.c_double, _d, _d,
+                           C.c_double, C.c_int, C.c_int, C.c_int, _d, C.POINTER(FktCgDiagnosticsC)),
+    "fkt_gp_posterior_mean": (C.c_int, C.c_int, C.c_int, _d, _d, _d, C.c_char_p, _cstrs, _d, C.c_int, C.c_int, _d,
+                              C.POINTER(FktGpOptionsC), _d, C.POINTER(FktCgDiagnosticsC)),
     "fkt_plan_kernel_launches": (C.c_longlong, C.c_void_p, C.c_int),
     "fkt_shard_cuts": (C.c_int, _u32, C.POINTER(C.c_ulonglong), C.c_int, C.c_int, C.c_uint32, _u32),
     "fkt_plan_tree": (C.c_void_p, C.c_void_p),

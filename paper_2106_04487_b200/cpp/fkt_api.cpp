@@ -8,6 +8,7 @@
 #include <mutex>
 #include <numeric>
 
+#include "fkt/gp.hpp"
 #include "fkt/kernels.hpp"
 #include "fkt/synthetic.hpp"
 #include "fkt/transform.hpp"
@@ -224,23 +225,30 @@ std::span<const double> PartitionTree::pointAt(std::uint32_t pos) const {
 }
 
 // ---------------------------------------------------------------------------
+namespace {
+fkt_options toC(const FktOptions& f) {
+  fkt_options o;
+  fkt_default_options(&o);
+  o.p = f.p;
+  o.theta = f.theta;
+  o.leaf_capacity = f.leafCapacity;
+  o.compression = f.compression == CompressionMode::On    ? FKT_COMPRESSION_ON
+                  : f.compression == CompressionMode::Off ? FKT_COMPRESSION_OFF
+                                                          : FKT_COMPRESSION_AUTO;
+  o.eager_operators = f.eagerOperators ? 1 : 0;
+  o.barnes_hut = f.barnesHut ? 1 : 0;
+  o.threads = f.threads;
+  o.has_diagonal = f.diagonal ? 1 : 0;
+  o.diagonal = f.diagonal.value_or(0.0);
+  o.near_precision = f.nearPrecision;
+  return o;
+}
+}  // namespace
+
 FktPlan::FktPlan(PointCloud cloud, KernelPtr kernel, const FktOptions& options)
     : cloud_(std::move(cloud)), kernel_(std::move(kernel)), options_(options) {
   requireBuiltin(*kernel_);
-  fkt_options o;
-  fkt_default_options(&o);
-  o.p = options_.p;
-  o.theta = options_.theta;
-  o.leaf_capacity = options_.leafCapacity;
-  o.compression = options_.compression == CompressionMode::On    ? FKT_COMPRESSION_ON
-                  : options_.compression == CompressionMode::Off ? FKT_COMPRESSION_OFF
-                                                                 : FKT_COMPRESSION_AUTO;
-  o.eager_operators = options_.eagerOperators ? 1 : 0;
-  o.barnes_hut = options_.barnesHut ? 1 : 0;
-  o.threads = options_.threads;
-  o.has_diagonal = options_.diagonal ? 1 : 0;
-  o.diagonal = options_.diagonal.value_or(0.0);
-  o.near_precision = options_.nearPrecision;
+  const fkt_options o = toC(options_);
   ParamArrays pa(kernel_->parameters());
   fkt_plan_t h = nullptr;
   check(fkt_plan_create(cloud_.n, cloud_.d, cloud_.x.data(), kernel_->name().c_str(), pa.k(), pa.v(), pa.n(), &o, &h));
@@ -425,6 +433,95 @@ std::vector<double> normalVector(int n, Rng& rng) {
   std::vector<double> v(static_cast<std::size_t>(n));
   for (double& e : v) e = rng.normal();
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian processes (reference gp.cpp:20-177) over the C-ABI's device CG.
+namespace {
+double safeDiagonal(const IsotropicKernel& k, const std::optional<double>& diagonal) {
+  // gp.cpp:10-16: kernel(0, diagonal), 0 when singular without a convention
+  if (diagonal) return *diagonal;
+  return k.valueAtZero().value_or(0.0);
+}
+CgDiagnostics fromC(const fkt_cg_diagnostics& d) {
+  CgDiagnostics out;
+  out.iterations = d.iterations;
+  out.finalResidual = d.final_residual;
+  out.converged = d.converged != 0;
+  out.restarts = d.restarts;
+  return out;
+}
+}  // namespace
+
+NoisyOperator::NoisyOperator(const FktPlan& plan, std::vector<double> noise)
+    : n_(plan.cloud().n), noise_(std::move(noise)), plan_(&plan), diagonal_(plan.options().diagonal) {
+  if (static_cast<int>(noise_.size()) != n_)
+    throw DimensionMismatchError("NoisyOperator: noise length does not match the point count");
+  kernelDiagonal_ = safeDiagonal(plan.kernel(), plan.options().diagonal);
+}
+
+NoisyOperator::NoisyOperator(const PointCloud& cloud, KernelPtr kernel, std::vector<double> noise,
+                             std::optional<double> diagonal)
+    : n_(cloud.n), noise_(std::move(noise)), cloud_(&cloud), kernel_(std::move(kernel)), diagonal_(diagonal) {
+  if (static_cast<int>(noise_.size()) != n_)
+    throw DimensionMismatchError("NoisyOperator: noise length does not match the point count");
+  requireBuiltin(*kernel_);
+  kernelDiagonal_ = safeDiagonal(*kernel_, diagonal);
+}
+
+std::vector<double> NoisyOperator::apply(std::span<const double> y) const {
+  if (static_cast<int>(y.size()) != n_) throw DimensionMismatchError("NoisyOperator: vector length mismatch");
+  std::vector<double> z = plan_ ? plan_->multiply(y) : denseMultiply(*cloud_, *kernel_, y, diagonal_);
+  for (int i = 0; i < n_; ++i) z[static_cast<std::size_t>(i)] += noise_[static_cast<std::size_t>(i)] * y[static_cast<std::size_t>(i)];
+  return z;
+}
+
+CgResult cgSolve(const NoisyOperator& op, std::span<const double> rhs, double tolerance, int maxIterations,
+                 bool jacobiPreconditioner, bool restartOnIncrease) {
+  if (!(tolerance > 0.0)) throw std::invalid_argument("cgSolve requires a positive tolerance");
+  if (static_cast<int>(rhs.size()) != op.size()) throw DimensionMismatchError("cgSolve: rhs length mismatch");
+  CgResult out;
+  out.x.resize(rhs.size());
+  fkt_cg_diagnostics d{};
+  if (op.plan()) {
+    check(fkt_cg_solve(static_cast<fkt_plan_t>(op.plan()->handle()), op.noise().data(), rhs.data(), tolerance,
+                       maxIterations, jacobiPreconditioner ? 1 : 0, restartOnIncrease ? 1 : 0, out.x.data(), &d));
+  } else {
+    const PointCloud& c = *op.cloud();
+    ParamArrays pa(op.kernelPtr()->parameters());
+    check(fkt_cg_solve_dense(c.n, c.d, c.x.data(), op.kernelPtr()->name().c_str(), pa.k(), pa.v(), pa.n(),
+                             op.diagonal() ? 1 : 0, op.diagonal().value_or(0.0), op.noise().data(), rhs.data(),
+                             tolerance, maxIterations, jacobiPreconditioner ? 1 : 0, restartOnIncrease ? 1 : 0,
+                             out.x.data(), &d));
+  }
+  out.diagnostics = fromC(d);
+  return out;
+}
+
+GpPrediction gpPosteriorMean(const PointCloud& train, std::span<const double> y, std::span<const double> noise,
+                             KernelPtr kernel, const PointCloud& test, const GpOptions& options) {
+  if (static_cast<int>(y.size()) != train.n || static_cast<int>(noise.size()) != train.n)
+    throw DimensionMismatchError("gpPosteriorMean: training vector lengths must match the cloud");
+  if (test.d != train.d) throw DimensionMismatchError("gpPosteriorMean: train/test dimension mismatch");
+  requireBuiltin(*kernel);
+  fkt_gp_options o;
+  fkt_default_gp_options(&o);
+  o.fkt = toC(options.fkt);
+  o.cg_tolerance = options.cgTolerance;
+  o.cg_max_iterations = options.cgMaxIterations;
+  o.jacobi = options.jacobiPreconditioner ? 1 : 0;
+  o.dense = options.dense ? 1 : 0;
+  o.has_prior_mean = options.priorMean ? 1 : 0;
+  o.prior_mean = options.priorMean.value_or(0.0);
+  o.restart_on_increase = options.restartOnIncrease ? 1 : 0;
+  ParamArrays pa(kernel->parameters());
+  GpPrediction pred;
+  pred.mean.resize(static_cast<std::size_t>(test.n));
+  fkt_cg_diagnostics d{};
+  check(fkt_gp_posterior_mean(train.n, train.d, train.x.data(), y.data(), noise.data(), kernel->name().c_str(), pa.k(),
+                              pa.v(), pa.n(), test.n, test.x.data(), &o, pred.mean.data(), &d));
+  pred.diagnostics = fromC(d);
+  return pred;
 }
 
 }  // namespace fkt

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/fkt_cuda.h"
+#include "gp.hpp"
 #include "plan.hpp"
 
 namespace fktb {
@@ -159,30 +160,49 @@ void fkt_default_options(fkt_options* o) {
   o->near_precision = 64;
 }
 
+}  // extern "C"
+
+namespace {
+fktb::PlanOptions toPlanOptions(const fkt_options* opt) {
+  fkt_options def;
+  fkt_default_options(&def);
+  const fkt_options& o = opt ? *opt : def;
+  fktb::PlanOptions po;
+  po.p = o.p;
+  po.theta = o.theta;
+  po.leafCapacity = o.leaf_capacity;
+  po.compression = o.compression;
+  po.eagerOperators = o.eager_operators != 0;
+  po.barnesHut = o.barnes_hut != 0;
+  po.threads = o.threads;
+  po.hasDiagonal = o.has_diagonal != 0;
+  po.diagonal = o.diagonal;
+  if (o.near_precision != 64 && o.near_precision != 32)
+    throw std::invalid_argument("near_precision must be 64 or 32");
+  po.nearPrecision = o.near_precision;
+  if (!po.barnesHut && po.p > fktb::kMaxExpansionOrder)
+    throw OrderTooLarge("expansion order " + std::to_string(po.p) + " exceeds the supported cap " +
+                        std::to_string(fktb::kMaxExpansionOrder));
+  return po;
+}
+
+void toC(const fktb::CgDiagnostics& d, fkt_cg_diagnostics* out) {
+  if (!out) return;
+  out->iterations = d.iterations;
+  out->final_residual = d.finalResidual;
+  out->converged = d.converged ? 1 : 0;
+  out->restarts = d.restarts;
+}
+}  // namespace
+
+extern "C" {
+
 int fkt_plan_create(int n, int d, const double* x, const char* kernel, const char* const* keys, const double* values,
                     int nparams, const fkt_options* opt, fkt_plan_t* out) {
   *out = nullptr;
   return guarded([&] {
     auto k = spec(kernel, keys, values, nparams);
-    fkt_options def;
-    fkt_default_options(&def);
-    const fkt_options& o = opt ? *opt : def;
-    fktb::PlanOptions po;
-    po.p = o.p;
-    po.theta = o.theta;
-    po.leafCapacity = o.leaf_capacity;
-    po.compression = o.compression;
-    po.eagerOperators = o.eager_operators != 0;
-    po.barnesHut = o.barnes_hut != 0;
-    po.threads = o.threads;
-    po.hasDiagonal = o.has_diagonal != 0;
-    po.diagonal = o.diagonal;
-    if (o.near_precision != 64 && o.near_precision != 32)
-      throw std::invalid_argument("near_precision must be 64 or 32");
-    po.nearPrecision = o.near_precision;
-    if (po.p > fktb::kMaxExpansionOrder)
-      throw OrderTooLarge("expansion order " + std::to_string(po.p) + " exceeds the supported cap " +
-                          std::to_string(fktb::kMaxExpansionOrder));
+    const fktb::PlanOptions po = toPlanOptions(opt);
     requireDevice();
     auto h = std::make_unique<fkt_plan_s>();
     h->plan = fktb::createPlan(n, d, x, k, po);
@@ -293,6 +313,98 @@ int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_
   return guarded([&] {
     *moments = plan->plan->dMoments.get();
     *count_per_rhs = static_cast<long long>(plan->plan->tree->nodes) * plan->plan->P;
+  });
+}
+
+void fkt_default_gp_options(fkt_gp_options* o) {
+  fkt_default_options(&o->fkt);
+  o->cg_tolerance = 1e-10;
+  o->cg_max_iterations = 1000;
+  o->jacobi = 0;
+  o->dense = 0;
+  o->has_prior_mean = 0;
+  o->prior_mean = 0.0;
+  o->restart_on_increase = 1;
+}
+
+int fkt_cg_solve(fkt_plan_t plan, const double* noise, const double* rhs, double tolerance, int max_iterations,
+                 int jacobi, int restart_on_increase, double* x, fkt_cg_diagnostics* diag) {
+  return guarded([&] {
+    auto& p = *plan->plan;
+    std::lock_guard<std::mutex> lock(p.mutex);
+    if (!(tolerance > 0.0)) throw std::invalid_argument("cgSolve requires a positive tolerance");
+    fktb::DeviceNoisyOperator op;
+    op.n = p.n;
+    op.plan = &p;
+    op.kernelDiagonal = fktb::safeKernelDiagonal(p.kernel, p.options.hasDiagonal, p.options.diagonal);
+    cudaStream_t st = p.stream;  // the plan's stream: its captured MVM graph is reused across solves
+    const size_t bytes = static_cast<size_t>(p.n) * sizeof(double);
+    op.noise.resize(static_cast<size_t>(p.n));
+    fktb::DeviceBuffer<double> dRhs(static_cast<size_t>(p.n)), dX(static_cast<size_t>(p.n));
+    FKTB_CUDA(cudaMemcpyAsync(op.noise.get(), noise, bytes, cudaMemcpyHostToDevice, st));
+    FKTB_CUDA(cudaMemcpyAsync(dRhs.get(), rhs, bytes, cudaMemcpyHostToDevice, st));
+    const auto d = fktb::cgSolveDevice(op, dRhs.get(), tolerance, max_iterations, jacobi != 0, dX.get(), st,
+                                       restart_on_increase != 0);
+    FKTB_CUDA(cudaMemcpyAsync(x, dX.get(), bytes, cudaMemcpyDeviceToHost, st));
+    FKTB_CUDA(cudaStreamSynchronize(st));
+    toC(d, diag);
+  });
+}
+
+int fkt_cg_solve_dense(int n, int d, const double* points, const char* kernel, const char* const* keys,
+                       const double* values, int nparams, int has_diagonal, double diagonal, const double* noise,
+                       const double* rhs, double tolerance, int max_iterations, int jacobi, int restart_on_increase,
+                       double* x, fkt_cg_diagnostics* diag) {
+  return guarded([&] {
+    auto k = spec(kernel, keys, values, nparams);
+    if (!(tolerance > 0.0)) throw std::invalid_argument("cgSolve requires a positive tolerance");
+    requireDevice();
+    cudaStream_t st;
+    FKTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      fktb::DeviceNoisyOperator op;
+      fktb::setupDenseOperator(op, n, d, points, k, has_diagonal != 0, diagonal, st);
+      op.kernelDiagonal = fktb::safeKernelDiagonal(k, has_diagonal != 0, diagonal);
+      const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+      op.noise.resize(static_cast<size_t>(n));
+      fktb::DeviceBuffer<double> dRhs(static_cast<size_t>(n)), dX(static_cast<size_t>(n));
+      FKTB_CUDA(cudaMemcpyAsync(op.noise.get(), noise, bytes, cudaMemcpyHostToDevice, st));
+      FKTB_CUDA(cudaMemcpyAsync(dRhs.get(), rhs, bytes, cudaMemcpyHostToDevice, st));
+      const auto dg = fktb::cgSolveDevice(op, dRhs.get(), tolerance, max_iterations, jacobi != 0, dX.get(), st,
+                                          restart_on_increase != 0);
+      FKTB_CUDA(cudaMemcpyAsync(x, dX.get(), bytes, cudaMemcpyDeviceToHost, st));
+      FKTB_CUDA(cudaStreamSynchronize(st));
+      toC(dg, diag);
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+  });
+}
+
+int fkt_gp_posterior_mean(int n_train, int d, const double* train_x, const double* y, const double* noise,
+                          const char* kernel, const char* const* keys, const double* values, int nparams, int n_test,
+                          const double* test_x, const fkt_gp_options* opt, double* mean, fkt_cg_diagnostics* diag) {
+  return guarded([&] {
+    auto k = spec(kernel, keys, values, nparams);
+    fkt_gp_options def;
+    fkt_default_gp_options(&def);
+    const fkt_gp_options& o = opt ? *opt : def;
+    fktb::GpDeviceOptions go;
+    go.fkt = toPlanOptions(&o.fkt);
+    go.cgTolerance = o.cg_tolerance;
+    go.cgMaxIterations = o.cg_max_iterations;
+    go.jacobi = o.jacobi != 0;
+    go.dense = o.dense != 0;
+    go.hasPriorMean = o.has_prior_mean != 0;
+    go.priorMean = o.prior_mean;
+    go.restartOnIncrease = o.restart_on_increase != 0;
+    if (n_train < 1) throw std::invalid_argument("point cloud must be nonempty");
+    if (n_test < 0) throw DimensionMismatch("gpPosteriorMean: negative test size");
+    requireDevice();
+    toC(fktb::gpPosteriorMeanGpu(n_train, d, train_x, y, noise, k, n_test, test_x, go, mean), diag);
   });
 }
 

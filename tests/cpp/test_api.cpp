@@ -9,6 +9,7 @@
 #include <string>
 
 #include "fkt/synthetic.hpp"
+#include "fkt/gp.hpp"
 #include "fkt/transform.hpp"
 
 static int g_fail = 0;
@@ -220,6 +221,39 @@ static void barnes_hut_baseline() {  // test_transform.cpp:188-222
   CHECK_THROWS_AS(barnesHutMultiply(plain, y), std::invalid_argument);
 }
 
+static void gp_pipeline() {  // test_gp.cpp:52-61, 115-123, 141-173 (textbook-CG intent)
+  Rng rng(17);
+  PointCloud train = cubeCloud(900, 2, rng);
+  PointCloud test = cubeCloud(100, 2, rng);
+  std::vector<double> y(900);
+  for (int i = 0; i < 900; ++i) y[static_cast<std::size_t>(i)] = std::sin(4.0 * train.point(i)[0]);
+  std::vector<double> noise(900, 0.01);
+  auto k = makeKernel("matern32");
+  NoisyOperator dense(train, k, noise);
+  std::vector<double> zero(900, 0.0);
+  const auto z0 = cgSolve(dense, zero, 1e-10, 50);
+  CHECK(z0.diagnostics.converged && z0.diagnostics.iterations == 0);
+  const auto sol = cgSolve(dense, y, 1e-10, 4000, false, false);
+  CHECK(sol.diagnostics.converged);
+  const auto ax = dense.apply(sol.x);
+  CHECK(relativeError(ax, y) <= 2e-10);
+  GpOptions o;
+  o.fkt.p = 12;
+  o.fkt.theta = 0.4;
+  o.fkt.leafCapacity = 256;
+  o.restartOnIncrease = false;
+  GpOptions od = o;
+  od.dense = true;
+  const auto pf = gpPosteriorMean(train, y, noise, k, test, o);
+  const auto pd = gpPosteriorMean(train, y, noise, k, test, od);
+  CHECK(pf.diagnostics.converged && pd.diagnostics.converged);
+  CHECK(relativeError(pf.mean, pd.mean) < 1e-4);
+  std::vector<double> c(900, 3.25);
+  for (double v : gpPosteriorMean(train, c, noise, k, test, {}).mean) CHECK(std::abs(v - 3.25) <= 1e-9);
+  std::vector<double> badNoise(899, 0.1);
+  CHECK_THROWS_AS(NoisyOperator(train, k, badNoise), DimensionMismatchError);
+}
+
 int main() {
   dense_basics();
   single_leaf_exact();
@@ -230,6 +264,7 @@ int main() {
   tree_structure();
   device_multiply_and_multi_rhs();
   barnes_hut_baseline();
+  gp_pipeline();
   std::printf("cpp api: %d failures\n", g_fail);
   return g_fail;
 }
