@@ -209,6 +209,15 @@ long long fkt_expansion_size(int d, int p);
  * kernel has no recurrence -> FKT_ERR_NOT_RECURRENCE); Z_k
  * (harmonics.hpp:56). */
 int fkt_tbar(int d, int p, int k, int j, int m, double* value, char* exact, int exact_len);
+/* CoefficientTable::serialize (coefficients.cpp:113-124): the exact T-bar
+ * table as text. Writes at most len bytes (NUL-terminated when len > 0) and
+ * returns the length needed including the NUL, -1 on error. Every plan also
+ * honours the reference's FKT_CACHE_DIR cache in this format. */
+long long fkt_tbar_serialize(int d, int p, char* buf, long long len);
+/* CoefficientTable::deserialize (:126-166): FKT_ERR_INVALID_ARGUMENT when the
+ * text does not parse (the reference returns nullopt); else d, p and whether
+ * the table equals the one computed here (operator==, :168-170). */
+int fkt_tbar_deserialize(const char* text, int* d, int* p, int* equals_computed);
 int fkt_compression_ranks(const char* kernel, const char* const* keys, const double* values, int nparams, int d,
                           int p, int* ranks);
 double fkt_addition_normalizer(int d, int k);

@@ -54,6 +54,8 @@ def lib():
             "fktref_addition_normalizer": (C.c_double, C.c_int, C.c_int),
             "fktref_harmonics": (C.c_int, C.c_int, C.c_int, d, d),
             "fktref_kernel_jet": (C.c_int, C.c_char_p, C.c_char_p, C.c_double, C.c_int, d),
+            "fktref_tbar_serialize": (C.c_longlong, C.c_int, C.c_int, C.c_char_p, C.c_longlong),
+            "fktref_tbar_deserialize": (C.c_int, C.c_char_p),
             "fktref_cg_solve": (C.c_int, C.c_int, C.c_int, d, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double,
                                 C.c_int, C.c_int, C.c_double, d, d, C.c_double, C.c_int, C.c_int, d, i32, d, i32,
                                 i32),
@@ -280,3 +282,18 @@ def gp_posterior_mean(train, y, noise, kernel, params, test, p=4, theta=0.75, le
                                       _dp(mean), C.byref(it), C.byref(res), C.byref(conv), C.byref(rs)) != 0:
         raise RuntimeError(lib().fktref_last_error().decode())
     return mean, _diag(it, res, conv, rs)
+
+
+def tbar_serialize(d: int, p: int) -> str:
+    """The reference CoefficientTable::serialize text (coefficients.cpp:113-124)."""
+    need = lib().fktref_tbar_serialize(d, p, None, 0)
+    if need < 0:
+        raise RuntimeError(lib().fktref_last_error().decode())
+    buf = C.create_string_buffer(int(need))
+    lib().fktref_tbar_serialize(d, p, buf, need)
+    return buf.value.decode()
+
+
+def tbar_deserialize(text: str) -> int:
+    """1: parses and equals the computed table; 0: parses, differs; -1: nullopt."""
+    return int(lib().fktref_tbar_deserialize(text.encode()))

@@ -412,6 +412,28 @@ int fktref_tbar(int d, int p, int k, int j, int m, double* value, char* buf, int
   }
 }
 
+// CoefficientTable::serialize (coefficients.cpp:113-124); returns the length
+// needed including the NUL.
+long long fktref_tbar_serialize(int d, int p, char* buf, long long len) {
+  try {
+    const std::string s = fkt::coefficientTable(d, p).serialize();
+    if (buf && len > 0) std::snprintf(buf, static_cast<std::size_t>(len), "%s", s.c_str());
+    return static_cast<long long>(s.size()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// CoefficientTable::deserialize (:126-166): 1 parses and equals the computed
+// table, 0 parses but differs, -1 nullopt.
+int fktref_tbar_deserialize(const char* text) {
+  auto t = fkt::CoefficientTable::deserialize(text);
+  if (!t) return -1;
+  if (t->maxOrder() > fkt::kMaxExpansionOrder) return 0;
+  return *t == fkt::coefficientTable(t->dimension(), t->maxOrder()) ? 1 : 0;
+}
+
 // Compression ranks per degree (expansion.cpp:190-243).
 int fktref_compression_ranks(const char* kernel, const char* params, int d, int p, int* ranks) {
   try {

@@ -674,6 +674,57 @@ def tbar(d: int, p: int, k: int, j: int, m: int):
     return v.value, buf.value.decode()
 
 
+class CoefficientTable:
+    """fkt::CoefficientTable (coefficients.hpp:43-76): the exact T-bar table,
+    its text serialization (coefficients.cpp:113-166) and equality."""
+
+    def __init__(self, d: int, p: int):
+        self._d, self._p = int(d), int(p)
+        if self._p > 20:
+            raise OrderTooLargeError(f"expansion order {p} exceeds the supported cap 20")
+
+    def dimension(self) -> int:
+        return self._d
+
+    def maxOrder(self) -> int:
+        return self._p
+
+    def tbar(self, k: int, j: int, m: int) -> str:
+        return tbar(self._d, self._p, k, j, m)[1]
+
+    def tbarDouble(self, k: int, j: int, m: int) -> float:
+        return tbar(self._d, self._p, k, j, m)[0]
+
+    def serialize(self) -> str:
+        need = lib.fkt_tbar_serialize(self._d, self._p, None, 0)
+        if need < 0:
+            _check(lib.fkt_last_error_code())
+        buf = C.create_string_buffer(int(need))
+        lib.fkt_tbar_serialize(self._d, self._p, buf, need)
+        return buf.value.decode()
+
+    @staticmethod
+    def deserialize(text: str) -> Optional["CoefficientTable"]:
+        """None when the text does not parse (as the reference's nullopt);
+        the table's (d, p) otherwise. `equalsComputed` tells whether it equals
+        the table computed here."""
+        d, p, eq = C.c_int(), C.c_int(), C.c_int()
+        if lib.fkt_tbar_deserialize(text.encode(), C.byref(d), C.byref(p), C.byref(eq)) != 0:
+            return None
+        t = CoefficientTable.__new__(CoefficientTable)
+        t._d, t._p = d.value, p.value
+        t.equalsComputed = bool(eq.value)
+        return t
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, CoefficientTable) and self.serialize() == other.serialize()
+
+
+def coefficientTable(d: int, p: int) -> CoefficientTable:
+    """fkt::coefficientTable (coefficients.cpp:210-213); FKT_CACHE_DIR honoured."""
+    return CoefficientTable(d, p)
+
+
 def compressionRanks(kernel: IsotropicKernel, d: int, p: int):
     ranks = (C.c_int * (p + 1))()
     k, v, n = _params(kernel.parameters())

@@ -126,6 +126,8 @@ SIGNATURES = {
     "fkt_relative_error": (C.c_int, _d, _d, C.c_longlong, _d),
     "fkt_expansion_size": (C.c_longlong, C.c_int, C.c_int),
     "fkt_tbar": (C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _d, C.c_char_p, C.c_int),
+    "fkt_tbar_serialize": (C.c_longlong, C.c_int, C.c_int, C.c_char_p, C.c_longlong),
+    "fkt_tbar_deserialize": (C.c_int, C.c_char_p, _i32, _i32, _i32),
     "fkt_compression_ranks": (C.c_int, C.c_char_p, _cstrs, _d, C.c_int, C.c_int, C.c_int, _i32),
     "fkt_addition_normalizer": (C.c_double, C.c_int, C.c_int),
     "fkt_harmonic_count": (C.c_longlong, C.c_int, C.c_int),

@@ -609,6 +609,34 @@ int fkt_tbar(int d, int p, int k, int j, int m, double* value, char* exact, int 
   });
 }
 
+long long fkt_tbar_serialize(int d, int p, char* buf, long long len) {
+  long long need = -1;
+  guarded([&] {
+    if (p > fktb::kMaxExpansionOrder)
+      throw OrderTooLarge("expansion order " + std::to_string(p) + " exceeds the supported cap " +
+                          std::to_string(fktb::kMaxExpansionOrder));
+    const std::string s = fktb::coefTable(d, p).serialize();
+    need = static_cast<long long>(s.size()) + 1;
+    if (buf && len > 0) {
+      const size_t n = static_cast<size_t>(std::min<long long>(len - 1, static_cast<long long>(s.size())));
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+  return need;
+}
+
+int fkt_tbar_deserialize(const char* text, int* d, int* p, int* equals_computed) {
+  return guarded([&] {
+    auto t = fktb::CoefTable::deserialize(text ? std::string(text) : std::string());
+    if (!t) throw std::invalid_argument("coefficient table text does not parse");
+    *d = t->dimension();
+    *p = t->maxOrder();
+    if (equals_computed) *equals_computed = t->maxOrder() <= fktb::kMaxExpansionOrder &&
+                                            *t == fktb::coefTable(t->dimension(), t->maxOrder());
+  });
+}
+
 int fkt_compression_ranks(const char* kernel, const char* const* keys, const double* values, int nparams, int d, int p,
                           int* ranks) {
   return guarded([&] {

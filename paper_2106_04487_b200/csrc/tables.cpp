@@ -2,8 +2,12 @@
 #include "tables.hpp"
 
 #include <cmath>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
 #include <memory>
 #include <mutex>
+#include <sstream>
 
 namespace fktb {
 
@@ -274,15 +278,8 @@ CoefTable::CoefTable(int d, int p) : d_(d), p_(p) {
   for (int n = 1; n <= p; ++n)
     for (int m = 1; m <= n; ++m) bell[static_cast<std::size_t>(n)].push_back(bellCoefficient(n, m));
   for (int i = 0; i <= p; ++i) cosp[static_cast<std::size_t>(i)] = cosinePowerCoefficients(d, i);
-  rowOffset_.assign(static_cast<std::size_t>(p) + 2, 0);
-  std::size_t rows = 0;
-  for (int k = 0; k <= p; ++k) {
-    rowOffset_[static_cast<std::size_t>(k)] = rows;
-    rows += static_cast<std::size_t>((p - k) / 2) + 1;
-  }
-  rowOffset_[static_cast<std::size_t>(p) + 1] = rows;
+  layout();
   const std::size_t w = static_cast<std::size_t>(std::max(p, 1));
-  t_.assign(rows * w, Rational(0));
   for (int k = 0; k <= p; ++k)
     for (int j = k; j <= p; j += 2)
       for (int m = 1; m <= j; ++m) {
@@ -300,6 +297,58 @@ CoefTable::CoefTable(int d, int p) : d_(d), p_(p) {
       }
   td_.resize(t_.size());
   for (std::size_t i = 0; i < t_.size(); ++i) td_[i] = toDouble(t_[i]);
+}
+
+void CoefTable::layout() {
+  rowOffset_.assign(static_cast<std::size_t>(p_) + 2, 0);
+  std::size_t rows = 0;
+  for (int k = 0; k <= p_; ++k) {
+    rowOffset_[static_cast<std::size_t>(k)] = rows;
+    rows += static_cast<std::size_t>((p_ - k) / 2) + 1;
+  }
+  rowOffset_[static_cast<std::size_t>(p_) + 1] = rows;
+  t_.assign(rows * static_cast<std::size_t>(std::max(p_, 1)), Rational(0));
+}
+
+std::string CoefTable::serialize() const {
+  std::ostringstream os;
+  os << "fkt-tbar 1 " << d_ << " " << p_ << "\n";
+  for (int k = 0; k <= p_; ++k)
+    for (int j = k; j <= p_; j += 2)
+      for (int m = 1; m <= j; ++m) {
+        const Rational& q = tbar(k, j, m);
+        os << k << " " << j << " " << m << " " << q.num() << " " << q.den() << "\n";
+      }
+  return os.str();
+}
+
+std::optional<CoefTable> CoefTable::deserialize(const std::string& text) {
+  std::istringstream is(text);
+  std::string magic;
+  int version = 0, d = 0, p = 0;
+  if (!(is >> magic >> version >> d >> p) || magic != "fkt-tbar" || version != 1) return std::nullopt;
+  if (d < 2 || p < 0 || p > kMaxInternalOrder) return std::nullopt;
+  CoefTable t;
+  t.d_ = d;
+  t.p_ = p;
+  t.layout();
+  const std::size_t w = static_cast<std::size_t>(std::max(p, 1));
+  int k, j, m;
+  BigInt num, den;
+  std::size_t count = 0;
+  while (is >> k >> j >> m >> num >> den) {
+    if (den.isZero()) return std::nullopt;
+    if (k < 0 || j < k || j > p || m < 1 || m > j || (j - k) % 2 != 0) return std::nullopt;
+    t.t_[t.row(k, j) * w + static_cast<std::size_t>(m - 1)] = Rational(num, den);
+    ++count;
+  }
+  std::size_t expected = 0;
+  for (int kk = 0; kk <= p; ++kk)
+    for (int jj = kk; jj <= p; jj += 2) expected += static_cast<std::size_t>(jj);
+  if (count != expected) return std::nullopt;
+  t.td_.resize(t.t_.size());
+  for (std::size_t i = 0; i < t.t_.size(); ++i) t.td_[i] = toDouble(t.t_[i]);
+  return t;
 }
 
 const Rational& CoefTable::tbar(int k, int j, int m) const {
@@ -321,7 +370,30 @@ const CoefTable& coefTable(int d, int p) {
   static std::map<std::pair<int, int>, std::unique_ptr<CoefTable>> tables;
   std::lock_guard<std::mutex> lock(mutex);
   auto& e = tables[{d, p}];
-  if (!e) e = std::make_unique<CoefTable>(d, p);
+  if (!e) {
+    // reference coefficients.cpp:170-214 (FKT_CACHE_DIR)
+    const char* dir = std::getenv("FKT_CACHE_DIR");
+    std::optional<std::filesystem::path> file;
+    if (dir && *dir)
+      file = std::filesystem::path(dir) / ("fkt-tbar-v1-d" + std::to_string(d) + "-p" + std::to_string(p) + ".txt");
+    if (file) {
+      std::ifstream in(*file);
+      if (in) {
+        std::stringstream buf;
+        buf << in.rdbuf();
+        if (auto loaded = CoefTable::deserialize(buf.str())) e = std::make_unique<CoefTable>(std::move(*loaded));
+      }
+    }
+    if (!e) {
+      e = std::make_unique<CoefTable>(d, p);
+      if (file) {
+        std::error_code ec;
+        std::filesystem::create_directories(file->parent_path(), ec);
+        std::ofstream out(*file);
+        if (out) out << e->serialize();
+      }
+    }
+  }
   return *e;
 }
 

@@ -86,16 +86,28 @@ class CoefTable {
   const Rational& tbar(int k, int j, int m) const;
   double tbarDouble(int k, int j, int m) const;
 
+  // Text format of the reference (coefficients.cpp:113-166): header
+  // "fkt-tbar 1 d p", then one "k j m num den" line per entry. deserialize
+  // returns nullopt on anything malformed, as the reference does.
+  std::string serialize() const;
+  static std::optional<CoefTable> deserialize(const std::string& text);
+  bool operator==(const CoefTable& o) const { return d_ == o.d_ && p_ == o.p_ && t_ == o.t_; }
+
  private:
+  CoefTable() = default;
+  void layout();
   std::size_t row(int k, int j) const { return rowOffset_[static_cast<std::size_t>(k)] + static_cast<std::size_t>((j - k) / 2); }
-  int d_, p_;
+  int d_ = 0, p_ = 0;
   std::vector<Rational> t_;
   std::vector<double> td_;
   std::vector<std::size_t> rowOffset_;
 };
 
-// Memoised, mutex-guarded (reference coefficients.cpp:187-220).
+// Memoised, mutex-guarded (reference coefficients.cpp:187-220); honours the
+// reference's FKT_CACHE_DIR on-disk cache (file fkt-tbar-v1-d<d>-p<p>.txt in
+// the serialize() format, read if it parses, written after a build).
 const CoefTable& coefTable(int d, int p);
+constexpr int kMaxInternalOrder = 32;  // reference coefficients.hpp:33
 
 // ---------------------------------------------------------------------------
 // Hyperspherical harmonics.
