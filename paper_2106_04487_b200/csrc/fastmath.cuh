@@ -3,9 +3,11 @@
 // The pair loop is bound by FP64-pipe issue, so these trade the last bits of
 // libm's correctly rounded results for fewer instructions while keeping a
 // relative error <= ~5e-14 per evaluation (z is gated at rel-L2 1e-10):
-//   * exp_neg(u) = e^-u, u >= 0: 64-entry 2^(j/64) table in shared memory,
-//     one-constant range reduction, degree-4 Taylor polynomial (|f| <=
-//     ln2/128), exponent added in the integer pipe. 8 FP64 ops.
+//   * exp_neg(u) = e^-u, u >= 0: 2^(j/2^BITS) table in shared memory,
+//     one-constant range reduction, Taylor polynomial (BITS = 6: 64 entries,
+//     degree 4, 8 FP64 ops -- the far kernels; BITS = 9: 512 entries, degree
+//     3, 7 FP64 ops -- the near field, measured -6.5% K3 time at cfg2),
+//     exponent added in the integer pipe.
 //   * rsqrt_nr / sqrt_nr: MUFU rsqrt.approx.f64 + one Newton step. 4 FP64 ops.
 //   * rcp_nr: MUFU rcp.approx.f64 + one Newton step. 2 FP64 ops.
 #ifndef FKTB_FASTMATH_CUH
@@ -64,29 +66,43 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y1, e1, y1);
 }
 
+// Near-field table: 2^NEAR_EXP_BITS entries (9 -> 512 entries, 4 KB of shared
+// memory, |f| <= ln2/1024 so a degree-3 polynomial suffices: one FP64 op per
+// pair fewer than the 64-entry / degree-4 table; cfg2 K3 14.72 -> 13.76 ms).
+#ifndef FKTB_NEAR_EXP_BITS
+#define FKTB_NEAR_EXP_BITS 9
+#endif
+constexpr int kNearExpBits = FKTB_NEAR_EXP_BITS;
+constexpr int kNearExpTable = 1 << kNearExpBits;
+
 // e^-u for u >= 0 (underflows to ~0 past u = 708). tab: the lane's column of
-// the replicated 2^(j/64) table (tab[j * kExpRep] = 2^(j/64)).
-template <int REP = kExpRep>
+// the replicated 2^(j/2^BITS) table (tab[j * REP] = 2^(j/2^BITS)).
+template <int REP = kExpRep, int BITS = 6>
 __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ tab) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  constexpr double kInvStep = 92.332482616893656;  // 64 / ln 2
-  // ln2/64 rounded to double: a one-constant reduction errs by |k| * 2^-60,
+  constexpr double kInvStep = 1.4426950408889634 * (1 << BITS);  // 2^BITS / ln 2 (exact power-of-two scaling)
+  // ln2/2^BITS rounded to double: a one-constant reduction errs by |k| * 2^-60,
   // i.e. <= u * 1e-16 relative in e^-u (a two-constant Cody-Waite step would
   // cost one more FP64 op per pair for accuracy the 1e-10 gate does not need).
-  constexpr double kStep = 0.010830424696249145;
+  constexpr double kStep = 0.6931471805599453 / (1 << BITS);
   // clamp u <= ~708 on the high word (integer pipe): e^-708 ~ 3e-308, and
   // keeps the exponent arithmetic below in the normal range
   u = __hiloint2double(min(__double2hiint(u), 0x40862000), __double2loint(u));
   const double t = fma(-u, kInvStep, kMagic);
-  const int k = __double2loint(t);  // round(-u * 64 / ln2), <= 0
+  const int k = __double2loint(t);  // round(-u * 2^BITS / ln2), <= 0
   const double kd = t - kMagic;
   const double f = fma(kd, -kStep, -u);
-  double p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
-  p = fma(f, p, 0.5);
+  double p;
+  if constexpr (BITS >= 9) {  // |f| <= 6.8e-4: degree 3, truncation f^4/24 < 9e-15
+    p = fma(f, 1.0 / 6.0, 0.5);
+  } else {  // |f| <= 5.4e-3: degree 4, truncation f^5/120 < 4e-14
+    p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
+    p = fma(f, p, 0.5);
+  }
   p = fma(f, p, 1.0);
   p = fma(f, p, 1.0);
-  const double tj = tab[(k & (kExpTable - 1)) * REP];
-  const int e = k >> 6;  // arithmetic shift: floor(k / 64)
+  const double tj = tab[(k & ((1 << BITS) - 1)) * REP];
+  const int e = k >> BITS;  // arithmetic shift: floor(k / 2^BITS)
   const double scaled = __hiloint2double(__double2hiint(tj) + (e << 20), __double2loint(tj));
   return scaled * p;
 }

@@ -126,10 +126,10 @@ __global__ void __launch_bounds__(THREADS) near_fast(const __grid_constant__ Fas
   constexpr int SP = (D + R + 1) / 2 * 2;  // AoS stride (coords + R weights), even
   constexpr int CHUNK = R > 2 ? 256 : kFastChunk;
   __shared__ __align__(16) double ss[CHUNK * SP];
-  __shared__ double tab[kExpTable];
+  __shared__ double tab[kNearExpTable];
   const NearArgs& A = F.a;
   if constexpr (FastKernel<KID>::needsTable)
-    for (int i = threadIdx.x; i < kExpTable; i += THREADS) tab[i] = F.expTable[i];
+    for (int i = threadIdx.x; i < kNearExpTable; i += THREADS) tab[i] = F.expTable[i];
   const FktbTile tile = A.tiles[blockIdx.x];
   const int leaf = tile.node;
   const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
@@ -234,7 +234,7 @@ void launchFastSel(const FastArgs& F, int nrhs, int tiles, cudaStream_t st) {
 
 template <int KID, int D>
 void launchFastT(const NearArgs& A, int tiles, cudaStream_t st) {
-  FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice()};
+  FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice(kNearExpBits)};
   fastScales(A.kd, F.sc, F.wf);
   F.diagCanon = A.kd.diag / F.wf;
   // The canonical formula already gives the reference convention at r == 0
@@ -281,17 +281,20 @@ void launchNearK(const NearArgs& A, int tiles, cudaStream_t st) {
 
 }  // namespace
 
-// 2^(j/64), j < 64, correctly rounded (host long double).
-const double* expTableDevice() {
-  static double* dev = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    double host[kExpTable];
-    for (int j = 0; j < kExpTable; ++j) host[j] = static_cast<double>(std::exp2(static_cast<long double>(j) / kExpTable));
-    FKTB_CUDA(cudaMalloc(&dev, sizeof(host)));
-    FKTB_CUDA(cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice));
+// 2^(j/2^bits), j < 2^bits, correctly rounded (host long double); one table
+// per size, built once (outside any graph capture: see createPlan).
+const double* expTableDevice(int bits) {
+  static double* dev[16] = {};
+  static std::once_flag once[16];
+  if (bits < 0 || bits >= 16) throw std::invalid_argument("exp table size");
+  std::call_once(once[bits], [bits] {
+    const int n = 1 << bits;
+    std::vector<double> host(static_cast<size_t>(n));
+    for (int j = 0; j < n; ++j) host[static_cast<size_t>(j)] = static_cast<double>(std::exp2(static_cast<long double>(j) / n));
+    FKTB_CUDA(cudaMalloc(&dev[bits], host.size() * sizeof(double)));
+    FKTB_CUDA(cudaMemcpy(dev[bits], host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
   });
-  return dev;
+  return dev[bits];
 }
 
 int nearTileSize() { return kNearThreads * kNearTPT; }

@@ -24,16 +24,16 @@ struct FastKernel {
   __device__ static __forceinline__ double eval(double q, const double* tab) {
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
       const double u = sqrt_nr(q);
-      const double e = exp_neg<REP>(u, tab);
+      const double e = exp_neg<REP, kNearExpBits>(u, tab);
       return fma(u, e, e);
     } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
-      return exp_neg<REP>(sqrt_nr(q), tab);
+      return exp_neg<REP, kNearExpBits>(sqrt_nr(q), tab);
     } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
       return rcp_nr(1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
       return rsqrt_nr(1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return exp_neg<REP>(q, tab);
+      return exp_neg<REP, kNearExpBits>(q, tab);
     } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
       return rsqrt_nr(q);
     } else {

@@ -133,9 +133,9 @@ __global__ void __launch_bounds__(kSymThreads, 10) near_block_kernel(const __gri
   constexpr int kOne = kSymChunk * SP, kSym = kSymChunkS * (SP + kZsStride);
   __shared__ __align__(16) double ss[kOne > kSym ? kOne : kSym];
   double* zs = ss + kSymChunkS * SP;
-  __shared__ double tab[kExpTable];
+  __shared__ double tab[kNearExpTable];
   if constexpr (FastKernel<KID>::needsTable)
-    for (int i = threadIdx.x; i < kExpTable; i += kSymThreads) tab[i] = A.expTable[i];
+    for (int i = threadIdx.x; i < kNearExpTable; i += kSymThreads) tab[i] = A.expTable[i];
   const FktbBlockTile tile = A.tiles[blockIdx.x];
   if (tile.sym)
     block_body<KID, D, SEL, true>(A, tile, ss, zs, tab);
@@ -296,7 +296,7 @@ bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrh
   FktbKernelDesc kd;
   fillKernelDesc(plan.kernel, kd);
   if (plan.options.hasDiagonal) kd.diag = plan.options.diagonal;
-  SymArgs A{plan.n, plan.tree->pc.get(), plan.dNearPool.get(), plan.dBlockTiles.get(), yp, zp, expTableDevice(),
+  SymArgs A{plan.n, plan.tree->pc.get(), plan.dNearPool.get(), plan.dBlockTiles.get(), yp, zp, expTableDevice(kNearExpBits),
             1.0, 1.0, 0.0};
   fastScales(kd, A.sc, A.wf);
   A.diagCanon = kd.diag / A.wf;

@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "device_math.cuh"
+#include "fastmath.cuh"
 #include "moments.hpp"
 #include "plan.hpp"
 
@@ -351,7 +352,8 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
-  (void)expTableDevice();  // lazy device table: initialise outside any graph capture
+  (void)expTableDevice();  // lazy device tables: initialise outside any graph capture
+  (void)expTableDevice(kNearExpBits);
   if (const char* g = std::getenv("FKTB_GRAPHS")) plan->useGraphs = std::atoi(g) != 0;
   FKTB_CUDA(cudaStreamSynchronize(plan->stream));
   plan->planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

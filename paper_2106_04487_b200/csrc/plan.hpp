@@ -177,8 +177,9 @@ void destroyPlan(DevicePlan* plan);
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
 
-// 2^(j/64), j < 64, in device memory (shared by the exp tables of every kernel).
-const double* expTableDevice();
+// 2^(j/2^bits), j < 2^bits, in device memory (default 64 entries: the far
+// kernels; the near field uses kNearExpBits).
+const double* expTableDevice(int bits = 6);
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
 // Multi-GPU target sharding (shard.cu).
