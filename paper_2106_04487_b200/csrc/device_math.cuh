@@ -331,6 +331,22 @@ constexpr int compressed_window_hi(int kid, int p) {
              : p;
 }
 
+// Compressed M2T, per kernel id: slots actually used per degree (the exact
+// rank of the radial compression, known per kernel family) and the per-degree
+// Laurent window of the target factors F_{k,i}. Laplace 1/r: rank 1 and
+// F_k ~ r^-k (the multipole series 1/|x-y| = sum_k r'^k / r^(k+1) P_k).
+// The host (buildFarParams) verifies the plan's factors against these before
+// the specialised kernel may run.
+constexpr int comp_slots(int kid, int p, int k) {
+  return kid == FKTB_KERNEL_INVERSE_R ? 1 : (p - k) / 2 + 1;
+}
+constexpr int comp_degree_lo(int kid, int p, int k) {
+  return kid == FKTB_KERNEL_INVERSE_R ? -k : compressed_window_lo(kid, p);
+}
+constexpr int comp_degree_hi(int kid, int p, int k) {
+  return kid == FKTB_KERNEL_INVERSE_R ? -k : compressed_window_hi(kid, p);
+}
+
 constexpr int harmonic_offset(int d, int k) {
   int h = 0;
   for (int q = 0; q < k; ++q) h += harmonic_count_deg(d, q);

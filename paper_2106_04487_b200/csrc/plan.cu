@@ -104,9 +104,14 @@ void buildFarParams(DevicePlan& plan) {
     fp->denseHi = compressed_window_hi(plan.kernel.id, p);
     const int span = fp->denseHi - fp->denseLo + 1;
     bool fits = c + f * span <= FKTB_FACTOR_CAP;
-    for (int k = 0; k <= p && fits; ++k)
+    // the specialised fused M2T reads rank <= comp_slots per degree, each
+    // factor over its degree window (device_math.cuh): verify here
+    for (int k = 0; k <= p && fits; ++k) {
+      const int kid = plan.kernel.id;
+      if (plan.factors[static_cast<size_t>(k)].rank > comp_slots(kid, p, k)) fits = false;
       for (const Laurent& F : plan.factors[static_cast<size_t>(k)].target)
-        if (F.minPower() < fp->denseLo || F.maxPower() > fp->denseHi) fits = false;
+        if (F.minPower() < comp_degree_lo(kid, p, k) || F.maxPower() > comp_degree_hi(kid, p, k)) fits = false;
+    }
     fp->denseAt = -1;
     if (fits) {
       fp->denseAt = c;
