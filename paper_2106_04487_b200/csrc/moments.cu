@@ -1,5 +1,8 @@
 // K4 source-to-multipole through monomial moments (see moments.hpp):
-//   K4a p2m   : leaves, mu_a = sum_src y x'^a  (x' about the leaf center)
+//   K4a p2m   : leaves, mu_a = sum_src y x'^a  (x' about the leaf center).
+//               Thread-owned (monomial, rhs) accumulators in registers;
+//               sources staged in shared memory as per-axis power tables,
+//               so each (source, item) is D broadcast loads + D multiplies.
 //   K4b m2m   : one launch per tree depth, bottom-up: parent mu from its two
 //               children's mu shifted by delta = c_child - c_parent
 //   K4c to_coef: per node with a far set, M = T mu (T carries Z_k nrm^2)
@@ -13,34 +16,12 @@ namespace fktb {
 namespace {
 
 constexpr int kP2MThreads = 128;
-constexpr int kRowPad = 1;  // odd per-lane row stride: conflict-free
 
 constexpr int mono_count(int dims, int rem) {
   // binom(dims + rem, rem)
   long long b = 1;
   for (int i = 1; i <= rem; ++i) b = b * (dims + i) / i;
   return static_cast<int>(b);
-}
-
-// row[IDX + j] += prod * x^a over the monomials of dims [A, D) with degree
-// <= REM, in the host enumeration order (MonomialBasis).
-template <int D, int A, int REM, int IDX>
-__device__ __forceinline__ void mono_accum(const double (&x)[D], double prod, double* row);
-
-template <int D, int A, int REM, int IDX, int E>
-__device__ __forceinline__ void mono_accum_e(const double (&x)[D], double prod, double* row) {
-  if constexpr (E <= REM) {
-    mono_accum<D, A + 1, REM - E, IDX>(x, prod, row);
-    mono_accum_e<D, A, REM, IDX + mono_count(D - A - 1, REM - E), E + 1>(x, prod * x[A], row);
-  }
-}
-
-template <int D, int A, int REM, int IDX>
-__device__ __forceinline__ void mono_accum(const double (&x)[D], double prod, double* row) {
-  if constexpr (A == D)
-    row[IDX] += prod;
-  else
-    mono_accum_e<D, A, REM, IDX, 0>(x, prod, row);
 }
 
 struct MomArgs {
@@ -65,36 +46,72 @@ struct MomArgs {
   double* moments;  // [rhs][node][P]
 };
 
-template <int D, int P>
-__global__ void __launch_bounds__(kP2MThreads, 1) p2m_kernel(const __grid_constant__ MomArgs A) {
+constexpr int kP2MChunk = 64;  // sources staged per pass
+
+// ITEMS accumulators per thread: items j = threadIdx.x + i * kP2MThreads,
+// item j = (rhs j / C, monomial j % C).
+template <int D, int P, int ITEMS>
+__global__ void __launch_bounds__(kP2MThreads) p2m_regs(const __grid_constant__ MomArgs A) {
   constexpr int C = mono_count(D, P);
-  extern __shared__ double rows[];  // [threads][nrhs * C + pad]
-  const int stride = C * A.nrhs + kRowPad;
+  constexpr int PW = P + 1;
+  __shared__ double spw[kP2MChunk * D * PW];  // [src][axis][power]
+  extern __shared__ double sw[];              // [src][rhs]
   const FktbTile tile = A.tiles[blockIdx.x];
   const int leaf = tile.node;
-  double* row = rows + static_cast<size_t>(threadIdx.x) * stride;
-  for (int i = 0; i < stride; ++i) row[i] = 0.0;
+  const int items = C * A.nrhs;
+  int off[ITEMS][D];  // offsets into one source's power table, per axis
+  int rr[ITEMS];
+  double acc[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int j = threadIdx.x + i * kP2MThreads;
+    const int a = j < items ? j % C : 0;
+    rr[i] = j < items ? j / C : -1;
+#pragma unroll
+    for (int q = 0; q < D; ++q) off[i][q] = q * PW + A.exps[a * D + q];
+    acc[i] = 0.0;
+  }
   double c[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) c[a] = A.center[static_cast<size_t>(leaf) * D + a];
-  for (int i = threadIdx.x; i < tile.count; i += kP2MThreads) {
-    const int pos = static_cast<int>(tile.start) + i;
-    double x[D];
+  for (int q = 0; q < D; ++q) c[q] = A.center[static_cast<size_t>(leaf) * D + q];
+  for (int s0 = 0; s0 < tile.count; s0 += kP2MChunk) {
+    const int cn = min(kP2MChunk, tile.count - s0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cn * D; t += kP2MThreads) {
+      const int s = t / D, q = t % D;
+      const int pos = static_cast<int>(tile.start) + s0 + s;
+      const double x = A.pc[static_cast<size_t>(q) * A.n + pos] - c[q];
+      double* row = spw + (s * D + q) * PW;
+      double v = 1.0;
+      row[0] = 1.0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) x[a] = A.pc[static_cast<size_t>(a) * A.n + pos] - c[a];
-    for (int r = 0; r < A.nrhs; ++r) mono_accum<D, 0, P, 0>(x, A.yp[static_cast<size_t>(r) * A.n + pos], row + r * C);
-  }
-  __syncthreads();
-  // column sums: warp w takes columns w, w+4, ...; lanes split the rows
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int col = warp; col < C * A.nrhs; col += kP2MThreads / 32) {
-    double s = 0.0;
-    for (int t = lane; t < kP2MThreads; t += 32) s += rows[static_cast<size_t>(t) * stride + col];
-    s = warp_sum(s);
-    if (lane == 0) {
-      const int r = col / C, a = col % C;
-      atomicAdd(A.mono + (static_cast<size_t>(r) * A.nodes + leaf) * C + a, s);
+      for (int e = 1; e <= P; ++e) {
+        v *= x;
+        row[e] = v;
+      }
     }
+    for (int t = threadIdx.x; t < cn * A.nrhs; t += kP2MThreads) {
+      const int s = t / A.nrhs, r = t % A.nrhs;
+      sw[t] = A.yp[static_cast<size_t>(r) * A.n + tile.start + s0 + s];
+    }
+    __syncthreads();
+    for (int s = 0; s < cn; ++s) {
+      const double* pw = spw + s * D * PW;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (rr[i] < 0) continue;
+        double m = sw[s * A.nrhs + rr[i]];
+#pragma unroll
+        for (int q = 0; q < D - 1; ++q) m *= pw[off[i][q]];
+        acc[i] = fma(m, pw[off[i][D - 1]], acc[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (rr[i] < 0) continue;
+    const int j = threadIdx.x + i * kP2MThreads;
+    atomicAdd(A.mono + (static_cast<size_t>(rr[i]) * A.nodes + leaf) * C + j % C, acc[i]);
   }
 }
 
@@ -152,12 +169,26 @@ __global__ void to_coef_kernel(const __grid_constant__ MomArgs A) {
   }
 }
 
+constexpr int kP2MMaxItems = 8;
+
 template <int D, int P>
 void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   constexpr int C = mono_count(D, P);
-  const size_t smem = static_cast<size_t>(kP2MThreads) * (C * A.nrhs + kRowPad) * sizeof(double);
-  FKTB_CUDA(cudaFuncSetAttribute(p2m_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  p2m_kernel<D, P><<<tiles, kP2MThreads, smem, st>>>(A);
+  const int per = (C * A.nrhs + kP2MThreads - 1) / kP2MThreads;
+  const size_t smem = static_cast<size_t>(kP2MChunk) * A.nrhs * sizeof(double);
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      FKTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<tiles, kP2MThreads, smem, st>>>(A);
+  };
+  if (per <= 1)
+    go(p2m_regs<D, P, 1>);
+  else if (per <= 2)
+    go(p2m_regs<D, P, 2>);
+  else if (per <= 4)
+    go(p2m_regs<D, P, 4>);
+  else
+    go(p2m_regs<D, P, kP2MMaxItems>);
   FKTB_CUDA(cudaGetLastError());
 }
 
@@ -206,9 +237,9 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   A.T = plan.dMomT.get();
   A.moments = moments;
   FKTB_CUDA(cudaMemsetAsync(plan.dMono.get(), 0, static_cast<size_t>(t.nodes) * C * nrhs * sizeof(double), st));
-  // K4a: per-lane rows must fit one CTA; chunk the right-hand sides.
-  const size_t perRhs = static_cast<size_t>(kP2MThreads) * C * sizeof(double);
-  const int chunk = std::max(1, static_cast<int>((200 * 1024) / perRhs));
+  // K4a: at most kP2MMaxItems register accumulators per thread; chunk the
+  // right-hand sides to fit.
+  const int chunk = std::max(1, kP2MMaxItems * kP2MThreads / C);
   const int tiles = static_cast<int>(plan.p2mTilesHost.size());
   for (int r0 = 0; r0 < nrhs && tiles > 0; r0 += chunk) {
     MomArgs B = A;

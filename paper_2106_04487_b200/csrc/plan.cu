@@ -387,7 +387,10 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
   };
   long long k = 2;  // gather_y, scatter_z
   if (plan.useMoments) {
-    if (!plan.p2mTilesHost.empty()) k += chunks(plan.monoCount);  // p2m
+    if (!plan.p2mTilesHost.empty()) {  // p2m: <= 8 x 128 register accumulators per launch
+      const int chunk = std::max(1, 8 * 128 / plan.monoCount);
+      k += (nrhs + chunk - 1) / chunk;
+    }
     for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
     k += !plan.farNodesHost.empty();  // to_coef
   } else if (!plan.s2mTilesHost.empty()) {
