@@ -5,7 +5,8 @@
 //               so each (source, item) is D broadcast loads + D multiplies.
 //   K4b m2m   : one launch per tree depth, bottom-up: parent mu from its two
 //               children's mu shifted by delta = c_child - c_parent
-//   K4c to_coef: per node with a far set, M = T mu (T carries Z_k nrm^2)
+//   K4c to_coef: M = T mu for every node as one small GEMM (T carries
+//               Z_k nrm^2 kappa^2; transposed copy for coalesced reads)
 // Compile-time (d, p) shapes only; other shapes keep the direct S2M (far.cu).
 #include <algorithm>
 
@@ -15,7 +16,6 @@
 namespace fktb {
 namespace {
 
-constexpr int kP2MThreads = 128;
 
 constexpr int mono_count(int dims, int rem) {
   // binom(dims + rem, rem)
@@ -46,38 +46,33 @@ struct MomArgs {
   double* moments;  // [rhs][node][P]
 };
 
-constexpr int kP2MChunk = 64;  // sources staged per pass
+constexpr int kP2MChunk = 64;     // sources staged per pass
+constexpr int kP2MMaxThreads = 1024;
 
-// ITEMS accumulators per thread: items j = threadIdx.x + i * kP2MThreads,
-// item j = (rhs j / C, monomial j % C).
-template <int D, int P, int ITEMS>
-__global__ void __launch_bounds__(kP2MThreads) p2m_regs(const __grid_constant__ MomArgs A) {
+// One (rhs, monomial) accumulator per thread: item j = threadIdx.x,
+// rhs j / C, monomial j % C (blockDim = C * nrhs rounded up to a warp).
+template <int D, int P>
+__global__ void __launch_bounds__(kP2MMaxThreads) p2m_regs(const __grid_constant__ MomArgs A) {
   constexpr int C = mono_count(D, P);
   constexpr int PW = P + 1;
   __shared__ double spw[kP2MChunk * D * PW];  // [src][axis][power]
   extern __shared__ double sw[];              // [src][rhs]
   const FktbTile tile = A.tiles[blockIdx.x];
   const int leaf = tile.node;
-  const int items = C * A.nrhs;
-  int off[ITEMS][D];  // offsets into one source's power table, per axis
-  int rr[ITEMS];
-  double acc[ITEMS];
+  const int j = threadIdx.x;
+  const bool active = j < C * A.nrhs;
+  const int a = active ? j % C : 0, rr = active ? j / C : 0;
+  int off[D];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int j = threadIdx.x + i * kP2MThreads;
-    const int a = j < items ? j % C : 0;
-    rr[i] = j < items ? j / C : -1;
-#pragma unroll
-    for (int q = 0; q < D; ++q) off[i][q] = q * PW + A.exps[a * D + q];
-    acc[i] = 0.0;
-  }
+  for (int q = 0; q < D; ++q) off[q] = q * PW + A.exps[a * D + q];
+  double acc = 0.0;
   double c[D];
 #pragma unroll
   for (int q = 0; q < D; ++q) c[q] = A.center[static_cast<size_t>(leaf) * D + q];
   for (int s0 = 0; s0 < tile.count; s0 += kP2MChunk) {
     const int cn = min(kP2MChunk, tile.count - s0);
     __syncthreads();
-    for (int t = threadIdx.x; t < cn * D; t += kP2MThreads) {
+    for (int t = threadIdx.x; t < cn * D; t += blockDim.x) {
       const int s = t / D, q = t % D;
       const int pos = static_cast<int>(tile.start) + s0 + s;
       const double x = A.pc[static_cast<size_t>(q) * A.n + pos] - c[q];
@@ -90,114 +85,122 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_regs(const __grid_constant__ 
         row[e] = v;
       }
     }
-    for (int t = threadIdx.x; t < cn * A.nrhs; t += kP2MThreads) {
+    for (int t = threadIdx.x; t < cn * A.nrhs; t += blockDim.x) {
       const int s = t / A.nrhs, r = t % A.nrhs;
       sw[t] = A.yp[static_cast<size_t>(r) * A.n + tile.start + s0 + s];
     }
     __syncthreads();
-    for (int s = 0; s < cn; ++s) {
-      const double* pw = spw + s * D * PW;
+    if (active) {
+#pragma unroll 4
+      for (int s = 0; s < cn; ++s) {
+        const double* pw = spw + s * D * PW;
+        double m = sw[s * A.nrhs + rr];
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        if (rr[i] < 0) continue;
-        double m = sw[s * A.nrhs + rr[i]];
-#pragma unroll
-        for (int q = 0; q < D - 1; ++q) m *= pw[off[i][q]];
-        acc[i] = fma(m, pw[off[i][D - 1]], acc[i]);
+        for (int q = 0; q < D - 1; ++q) m *= pw[off[q]];
+        acc = fma(m, pw[off[D - 1]], acc);
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    if (rr[i] < 0) continue;
-    const int j = threadIdx.x + i * kP2MThreads;
-    atomicAdd(A.mono + (static_cast<size_t>(rr[i]) * A.nodes + leaf) * C + j % C, acc[i]);
-  }
+  if (active) atomicAdd(A.mono + (static_cast<size_t>(rr) * A.nodes + leaf) * C + a, acc);
 }
 
+// Shift tables (CSR over the output monomial) staged in shared memory once
+// per CTA; each CTA then walks parents blockIdx.x, blockIdx.x + gridDim.x, ...
 template <int D>
-__global__ void m2m_kernel(const __grid_constant__ MomArgs A) {
-  extern __shared__ double sm[];  // dpow[2][count], mu[2][nrhs][count]
+__global__ void m2m_kernel(const __grid_constant__ MomArgs A, int parents, int entries) {
+  extern __shared__ double sm[];  // coef[E] | dpow[2][C] | mu[2][nrhs][C] | off[C+1] b[E] g[E] (ints)
   const int C = A.count;
-  const int parent = A.levelNodes[blockIdx.x];
-  const int kids[2] = {A.left[parent], A.right[parent]};
-  double* dpow = sm;
-  double* mu = sm + 2 * C;
-  for (int i = threadIdx.x; i < 2 * C; i += blockDim.x) {
-    const int ch = i / C, a = i % C;
-    double v = 1.0;
+  double* scoef = sm;
+  double* dpow = scoef + entries;
+  double* mu = dpow + 2 * C;
+  int* soff = reinterpret_cast<int*>(mu + 2 * A.nrhs * C);
+  int* sb = soff + C + 1;
+  int* sg = sb + entries;
+  for (int i = threadIdx.x; i < entries; i += blockDim.x) {
+    scoef[i] = A.coef[i];
+    sb[i] = A.b[i];
+    sg[i] = A.g[i];
+  }
+  for (int i = threadIdx.x; i <= C; i += blockDim.x) soff[i] = A.off[i];
+  for (int pi = blockIdx.x; pi < parents; pi += gridDim.x) {
+    const int parent = A.levelNodes[pi];
+    const int kids[2] = {A.left[parent], A.right[parent]};
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * C; i += blockDim.x) {
+      const int ch = i / C, a = i % C;
+      double v = 1.0;
 #pragma unroll
-    for (int q = 0; q < D; ++q) {
-      const double delta = A.center[static_cast<size_t>(kids[ch]) * D + q] - A.center[static_cast<size_t>(parent) * D + q];
-      for (int e = 0; e < A.exps[a * D + q]; ++e) v *= delta;
+      for (int q = 0; q < D; ++q) {
+        const double delta =
+            A.center[static_cast<size_t>(kids[ch]) * D + q] - A.center[static_cast<size_t>(parent) * D + q];
+        for (int e = 0; e < A.exps[a * D + q]; ++e) v *= delta;
+      }
+      dpow[i] = v;
     }
-    dpow[i] = v;
-  }
-  for (int i = threadIdx.x; i < 2 * A.nrhs * C; i += blockDim.x) {
-    const int ch = i / (A.nrhs * C), rem = i % (A.nrhs * C), r = rem / C, a = rem % C;
-    mu[i] = A.mono[(static_cast<size_t>(r) * A.nodes + kids[ch]) * C + a];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < A.nrhs * C; i += blockDim.x) {
-    const int r = i / C, a = i % C;
-    double acc = 0.0;
-    for (int ch = 0; ch < 2; ++ch) {
-      const double* dp = dpow + ch * C;
-      const double* m = mu + (static_cast<size_t>(ch) * A.nrhs + r) * C;
-      for (int e = A.off[a]; e < A.off[a + 1]; ++e) acc = fma(A.coef[e] * dp[A.g[e]], m[A.b[e]], acc);
+    for (int i = threadIdx.x; i < 2 * A.nrhs * C; i += blockDim.x) {
+      const int ch = i / (A.nrhs * C), rem = i % (A.nrhs * C), r = rem / C, a = rem % C;
+      mu[i] = A.mono[(static_cast<size_t>(r) * A.nodes + kids[ch]) * C + a];
     }
-    A.mono[(static_cast<size_t>(r) * A.nodes + parent) * C + a] = acc;
+    __syncthreads();
+    for (int i = threadIdx.x; i < A.nrhs * C; i += blockDim.x) {
+      const int r = i / C, a = i % C;
+      double acc = 0.0;
+      for (int ch = 0; ch < 2; ++ch) {
+        const double* dp = dpow + ch * C;
+        const double* m = mu + (static_cast<size_t>(ch) * A.nrhs + r) * C;
+        for (int e = soff[a]; e < soff[a + 1]; ++e) acc = fma(scoef[e] * dp[sg[e]], m[sb[e]], acc);
+      }
+      A.mono[(static_cast<size_t>(r) * A.nodes + parent) * C + a] = acc;
+    }
   }
 }
 
-__global__ void to_coef_kernel(const __grid_constant__ MomArgs A) {
-  extern __shared__ double mu[];  // [nrhs][count]
-  const int C = A.count;
-  const int node = A.farNodes[blockIdx.x];
-  for (int i = threadIdx.x; i < A.nrhs * C; i += blockDim.x) {
-    const int r = i / C, a = i % C;
-    mu[i] = A.mono[(static_cast<size_t>(r) * A.nodes + node) * C + a];
+// Node moments in the FKT basis for every (rhs, node) row: out[R][P] =
+// mono[R][C] * TT[C][P] -- a small GEMM, 32 rows per CTA staged in shared
+// memory, TT columns read coalesced (same for every CTA: L1/L2 resident).
+constexpr int kTcRows = 32;
+__global__ void __launch_bounds__(128) to_coef_gemm(const double* mono, const double* TT, double* out, int R, int C,
+                                                   int P) {
+  extern __shared__ double smu[];  // [kTcRows][C + 1]
+  const int r0 = blockIdx.x * kTcRows;
+  const int rows = min(kTcRows, R - r0);
+  for (int i = threadIdx.x; i < rows * C; i += blockDim.x) {
+    const int rr = i / C, a = i % C;
+    smu[rr * (C + 1) + a] = mono[static_cast<size_t>(r0 + rr) * C + a];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < A.nrhs * A.P; i += blockDim.x) {
-    const int r = i / A.P, c = i % A.P;
-    const double* t = A.T + static_cast<size_t>(c) * C;
-    const double* m = mu + static_cast<size_t>(r) * C;
-    double acc = 0.0;
-    for (int a = 0; a < C; ++a) acc = fma(t[a], m[a], acc);
-    A.moments[(static_cast<size_t>(r) * A.nodes + node) * A.P + c] = acc;
+  for (int c = threadIdx.x; c < P; c += blockDim.x) {
+    double acc[kTcRows];
+#pragma unroll
+    for (int i = 0; i < kTcRows; ++i) acc[i] = 0.0;
+    for (int a = 0; a < C; ++a) {
+      const double t = TT[static_cast<size_t>(a) * P + c];
+#pragma unroll
+      for (int i = 0; i < kTcRows; ++i) acc[i] = fma(t, smu[i * (C + 1) + a], acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kTcRows; ++i)
+      if (i < rows) out[static_cast<size_t>(r0 + i) * P + c] = acc[i];
   }
 }
-
-constexpr int kP2MMaxItems = 8;
 
 template <int D, int P>
 void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   constexpr int C = mono_count(D, P);
-  const int per = (C * A.nrhs + kP2MThreads - 1) / kP2MThreads;
+  const int threads = std::min(kP2MMaxThreads, (C * A.nrhs + 31) / 32 * 32);
   const size_t smem = static_cast<size_t>(kP2MChunk) * A.nrhs * sizeof(double);
-  auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      FKTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<tiles, kP2MThreads, smem, st>>>(A);
-  };
-  if (per <= 1)
-    go(p2m_regs<D, P, 1>);
-  else if (per <= 2)
-    go(p2m_regs<D, P, 2>);
-  else if (per <= 4)
-    go(p2m_regs<D, P, 4>);
-  else
-    go(p2m_regs<D, P, kP2MMaxItems>);
+  p2m_regs<D, P><<<tiles, threads, smem, st>>>(A);
   FKTB_CUDA(cudaGetLastError());
 }
 
 template <int D>
-void launchM2M(const MomArgs& A, int parents, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(2 * A.count * (1 + A.nrhs)) * sizeof(double);
+void launchM2M(const MomArgs& A, int parents, int entries, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(entries + 2 * A.count * (1 + A.nrhs)) * sizeof(double) +
+                      static_cast<size_t>(A.count + 1 + 2 * entries) * sizeof(int);
   if (smem > 48 * 1024)
     FKTB_CUDA(cudaFuncSetAttribute(m2m_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  m2m_kernel<D><<<parents, 128, smem, st>>>(A);
+  const int grid = std::min(parents, 148 * 2);
+  m2m_kernel<D><<<grid, 256, smem, st>>>(A, parents, entries);
   FKTB_CUDA(cudaGetLastError());
 }
 
@@ -237,9 +240,9 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   A.T = plan.dMomT.get();
   A.moments = moments;
   FKTB_CUDA(cudaMemsetAsync(plan.dMono.get(), 0, static_cast<size_t>(t.nodes) * C * nrhs * sizeof(double), st));
-  // K4a: at most kP2MMaxItems register accumulators per thread; chunk the
+  // K4a: one accumulator per thread, at most kP2MMaxThreads per CTA; chunk the
   // right-hand sides to fit.
-  const int chunk = std::max(1, kP2MMaxItems * kP2MThreads / C);
+  const int chunk = std::max(1, kP2MMaxThreads / C);
   const int tiles = static_cast<int>(plan.p2mTilesHost.size());
   for (int r0 = 0; r0 < nrhs && tiles > 0; r0 += chunk) {
     MomArgs B = A;
@@ -264,19 +267,20 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
     MomArgs B = A;
     B.levelNodes = plan.dLevelNodes.get() + a0;
     switch (plan.d) {
-      case 2: launchM2M<2>(B, a1 - a0, st); break;
-      case 3: launchM2M<3>(B, a1 - a0, st); break;
-      case 5: launchM2M<5>(B, a1 - a0, st); break;
+      case 2: launchM2M<2>(B, a1 - a0, plan.shiftEntries, st); break;
+      case 3: launchM2M<3>(B, a1 - a0, plan.shiftEntries, st); break;
+      case 5: launchM2M<5>(B, a1 - a0, plan.shiftEntries, st); break;
       default: throw std::logic_error("monomial S2M: unsupported dimension");
     }
   }
-  // K4c: node moments in the FKT basis.
-  const int farNodes = static_cast<int>(plan.farNodesHost.size());
-  if (farNodes > 0) {
-    const size_t smem = static_cast<size_t>(nrhs) * C * sizeof(double);
+  // K4c: node moments in the FKT basis, every (rhs, node) row at once.
+  if (!plan.farNodesHost.empty()) {
+    const int R = nrhs * t.nodes;
+    const size_t smem = static_cast<size_t>(kTcRows) * (C + 1) * sizeof(double);
     if (smem > 48 * 1024)
-      FKTB_CUDA(cudaFuncSetAttribute(to_coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    to_coef_kernel<<<farNodes, 128, smem, st>>>(A);
+      FKTB_CUDA(cudaFuncSetAttribute(to_coef_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    to_coef_gemm<<<(R + kTcRows - 1) / kTcRows, 128, smem, st>>>(plan.dMono.get(), plan.dMomTT.get(), moments, R, C,
+                                                               plan.P);
     FKTB_CUDA(cudaGetLastError());
   }
 }

@@ -220,6 +220,15 @@ void buildMomentPlan(DevicePlan& plan) {
   plan.monoCount = mt.count;
   cudaStream_t st = plan.stream;
   uploadVec(plan.dMomT, mt.T, st);
+  {
+    std::vector<double> tt(mt.T.size());
+    const size_t Pn = mt.T.size() / static_cast<size_t>(mt.count);
+    for (size_t c = 0; c < Pn; ++c)
+      for (size_t a = 0; a < static_cast<size_t>(mt.count); ++a) tt[a * Pn + c] = mt.T[c * mt.count + a];
+    uploadVec(plan.dMomTT, tt, st);
+    FKTB_CUDA(cudaStreamSynchronize(st));  // tt is a host temporary
+  }
+  plan.shiftEntries = static_cast<int>(mt.b.size());
   uploadVec(plan.dShiftOff, mt.off, st);
   uploadVec(plan.dShiftB, mt.b, st);
   uploadVec(plan.dShiftG, mt.g, st);
@@ -392,7 +401,7 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
       k += (nrhs + chunk - 1) / chunk;
     }
     for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
-    k += !plan.farNodesHost.empty();  // to_coef
+    k += !plan.farNodesHost.empty();  // to_coef (one GEMM over all nodes)
   } else if (!plan.s2mTilesHost.empty()) {
     k += plan.options.barnesHut ? 1 : chunks(plan.P);
   }

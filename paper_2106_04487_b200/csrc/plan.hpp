@@ -145,7 +145,8 @@ struct DevicePlan {
   bool useMoments = false;
   int monoCount = 0;
   std::vector<double> hscaleHost, kappaHost;
-  DeviceBuffer<double> dMono, dMomT, dShiftCoef;
+  DeviceBuffer<double> dMono, dMomT, dMomTT, dShiftCoef;  // dMomTT: T transposed, count x P
+  int shiftEntries = 0;
   DeviceBuffer<int> dShiftOff, dShiftB, dShiftG, dMonoExps, dLevelNodes, dFarNodes;
   std::vector<FktbTile> p2mTilesHost;
   DeviceBuffer<FktbTile> dP2mTiles;
