@@ -1,2 +1,4 @@
-for c in 5; do echo "cfg$c"; SWEEP_CFG=$c python scripts/sweep_near.py 0; done
-timeout 900 python -m pytest tests/test_gpu_full.py tests/test_gpu_reference_suite.py tests/test_gpu_parity.py -q -x -k "rhs or cfg5 or multi or parity" 2>&1 | tail -3
+timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+mkdir -p gpurun_out
+bash scripts/gpu_bench_all.sh
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 400 gpurun_out/bench_default.json
