@@ -91,6 +91,19 @@ int fkt_plan_create(int n, int d, const double* x, const char* kernel, const cha
 int fkt_plan_destroy(fkt_plan_t plan);
 int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info);
 
+/* Plan cache (the reference rebuilds a plan per call site, e.g.
+ * gp.cpp:148-151, 162-168). Returns a plan for (x, kernel, options), built
+ * only when no identical plan (same coordinates bytewise, kernel, parameters
+ * and options) is cached; *hit tells which. Every get must be paired with a
+ * release (fkt_plan_destroy refuses cached plans). Unreferenced plans stay
+ * cached up to the capacity (default 4) and are evicted least recently used
+ * first. Cached plans are shared: do not fkt_plan_set_shard them. */
+int fkt_plan_cache_get(int n, int d, const double* x, const char* kernel, const char* const* keys,
+                       const double* values, int nparams, const fkt_options* opt, fkt_plan_t* out, int* hit);
+int fkt_plan_cache_release(fkt_plan_t plan);
+int fkt_plan_cache_set_capacity(int plans);
+int fkt_plan_cache_size(void);
+
 /* fkt::FktPlan::multiply(span y) — transform.cpp:184-204. Host buffers,
  * synchronous; nrhs column-major right-hand sides (length n*nrhs). */
 int fkt_plan_multiply(fkt_plan_t plan, const double* y, double* z, int nrhs);

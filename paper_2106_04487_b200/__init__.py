@@ -351,7 +351,8 @@ class PartitionTree:
 class FktPlan:
     """fkt::FktPlan (transform.hpp:43-74) on one GPU."""
 
-    def __init__(self, cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None):
+    def __init__(self, cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None,
+                 _cached: bool = False):
         options = options or FktOptions()
         self._cloud = PointCloud(cloud.n, cloud.d, cloud.x.copy())
         self._kernel = kernel
@@ -364,8 +365,16 @@ class FktPlan:
         h = C.c_void_p()
         k, v, n = _params(kernel.parameters())
         oc = options._c()
-        _check(lib.fkt_plan_create(cloud.n, cloud.d, _dptr(self._cloud.x), kernel.name().encode(), k, v, n,
-                                   C.byref(oc), C.byref(h)))
+        self._cached = _cached
+        self.cacheHit = False
+        if _cached:
+            hit = C.c_int()
+            _check(lib.fkt_plan_cache_get(cloud.n, cloud.d, _dptr(self._cloud.x), kernel.name().encode(), k, v, n,
+                                          C.byref(oc), C.byref(h), C.byref(hit)))
+            self.cacheHit = bool(hit.value)
+        else:
+            _check(lib.fkt_plan_create(cloud.n, cloud.d, _dptr(self._cloud.x), kernel.name().encode(), k, v, n,
+                                       C.byref(oc), C.byref(h)))
         self._h = h
         self._tree = None
         info = _L.FktPlanInfoC()
@@ -375,7 +384,10 @@ class FktPlan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib.fkt_plan_destroy(h)
+            if getattr(self, "_cached", False):
+                lib.fkt_plan_cache_release(h)
+            else:
+                lib.fkt_plan_destroy(h)
             self._h = None
 
     def close(self):
@@ -487,6 +499,21 @@ def barnesHutMultiply(plan: FktPlan, y) -> np.ndarray:
     if not plan.options().barnesHut:
         raise InvalidArgument("barnesHutMultiply requires a plan built with the Barnes-Hut option")
     return plan.multiply(y)
+
+
+def cachedPlan(cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None) -> FktPlan:
+    """A plan from the library's plan cache (fkt_plan_cache_get): identical
+    (cloud, kernel, options) requests share one device plan; `.cacheHit` says
+    whether it was reused. The reference rebuilds plans per call site."""
+    return FktPlan(cloud, kernel, options, _cached=True)
+
+
+def planCacheCapacity(plans: int) -> None:
+    _check(lib.fkt_plan_cache_set_capacity(int(plans)))
+
+
+def planCacheSize() -> int:
+    return int(lib.fkt_plan_cache_size())
 
 
 def denseMultiply(cloud: PointCloud, kernel: IsotropicKernel, y, diagonal: Optional[float] = None,

@@ -93,6 +93,11 @@ SIGNATURES = {
     "fkt_plan_create": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int,
                         C.POINTER(FktOptionsC), C.POINTER(C.c_void_p)),
     "fkt_plan_destroy": (C.c_int, C.c_void_p),
+    "fkt_plan_cache_get": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int, C.POINTER(FktOptionsC),
+                           C.POINTER(C.c_void_p), _i32),
+    "fkt_plan_cache_release": (C.c_int, C.c_void_p),
+    "fkt_plan_cache_set_capacity": (C.c_int, C.c_int),
+    "fkt_plan_cache_size": (C.c_int,),
     "fkt_plan_info_get": (C.c_int, C.c_void_p, C.POINTER(FktPlanInfoC)),
     "fkt_plan_multiply": (C.c_int, C.c_void_p, _d, _d, C.c_int),
     "fkt_plan_multiply_device": (C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p),

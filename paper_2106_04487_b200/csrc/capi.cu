@@ -19,6 +19,8 @@ int configDims(int cfg, int* d, int* nrhs);
 
 struct fkt_plan_s {
   std::unique_ptr<fktb::DevicePlan> plan;
+  bool cached = false;  // owned by the plan cache (fkt_plan_cache_get)
+  int refs = 0;         // outstanding fkt_plan_cache_get references
 };
 struct fkt_tree_s {
   fktb::DeviceTree* tree = nullptr;   // borrowed or owned
@@ -213,10 +215,124 @@ int fkt_plan_create(int n, int d, const double* x, const char* kernel, const cha
 int fkt_plan_destroy(fkt_plan_t plan) {
   return guarded([&] {
     if (!plan) return;
+    if (plan->cached) throw std::invalid_argument("plan is owned by the plan cache: use fkt_plan_cache_release");
     fktb::DevicePlan* p = plan->plan.release();
     fktb::destroyPlan(p);
     delete plan;
   });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Plan cache: identical (cloud, kernel, options) requests share
+// one device plan. Entries are matched on the full inputs (the coordinates
+// are compared bytewise, not only hashed); unreferenced plans are kept up to
+// the capacity and evicted least-recently-used first.
+namespace {
+struct CacheEntry {
+  int n = 0, d = 0;
+  std::vector<double> x;
+  std::string kernel;
+  std::map<std::string, double> params;
+  fkt_options opt{};
+  fkt_plan_t plan = nullptr;
+  unsigned long long lastUse = 0;
+};
+std::mutex g_cacheMutex;
+std::vector<CacheEntry> g_cache;
+int g_cacheCapacity = 4;
+unsigned long long g_cacheClock = 0;
+
+bool sameOptions(const fkt_options& a, const fkt_options& b) {
+  return a.p == b.p && a.theta == b.theta && a.leaf_capacity == b.leaf_capacity && a.compression == b.compression &&
+         a.barnes_hut == b.barnes_hut && a.has_diagonal == b.has_diagonal &&
+         (!a.has_diagonal || a.diagonal == b.diagonal) && a.near_precision == b.near_precision;
+}
+
+void evictLocked() {
+  // drop unreferenced entries, oldest first, while over capacity
+  while (true) {
+    int unref = 0;
+    for (const auto& e : g_cache) unref += e.plan->refs == 0;
+    if (static_cast<int>(g_cache.size()) <= g_cacheCapacity || unref == 0) return;
+    auto victim = g_cache.end();
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if (it->plan->refs == 0 && (victim == g_cache.end() || it->lastUse < victim->lastUse)) victim = it;
+    fktb::DevicePlan* p = victim->plan->plan.release();
+    fktb::destroyPlan(p);
+    delete victim->plan;
+    g_cache.erase(victim);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int fkt_plan_cache_get(int n, int d, const double* x, const char* kernel, const char* const* keys,
+                       const double* values, int nparams, const fkt_options* opt, fkt_plan_t* out, int* hit) {
+  *out = nullptr;
+  return guarded([&] {
+    auto k = spec(kernel, keys, values, nparams);
+    fkt_options o;
+    fkt_default_options(&o);
+    if (opt) o = *opt;
+    const auto params = toParams(keys, values, nparams);
+    std::lock_guard<std::mutex> lock(g_cacheMutex);
+    for (auto& e : g_cache) {
+      if (e.n == n && e.d == d && e.kernel == kernel && e.params == params && sameOptions(e.opt, o) &&
+          std::memcmp(e.x.data(), x, static_cast<size_t>(n) * d * sizeof(double)) == 0) {
+        ++e.plan->refs;
+        e.lastUse = ++g_cacheClock;
+        *out = e.plan;
+        if (hit) *hit = 1;
+        return;
+      }
+    }
+    const fktb::PlanOptions po = toPlanOptions(&o);
+    requireDevice();
+    auto h = std::make_unique<fkt_plan_s>();
+    h->plan = fktb::createPlan(n, d, x, k, po);
+    h->cached = true;
+    h->refs = 1;
+    CacheEntry e;
+    e.n = n;
+    e.d = d;
+    e.x.assign(x, x + static_cast<size_t>(n) * d);
+    e.kernel = kernel;
+    e.params = params;
+    e.opt = o;
+    e.plan = h.release();
+    e.lastUse = ++g_cacheClock;
+    g_cache.push_back(std::move(e));
+    *out = g_cache.back().plan;
+    if (hit) *hit = 0;
+    evictLocked();
+  });
+}
+
+int fkt_plan_cache_release(fkt_plan_t plan) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(g_cacheMutex);
+    if (!plan || !plan->cached) throw std::invalid_argument("plan was not obtained from the plan cache");
+    if (plan->refs <= 0) throw std::invalid_argument("plan cache reference released twice");
+    --plan->refs;
+    evictLocked();
+  });
+}
+
+int fkt_plan_cache_set_capacity(int plans) {
+  return guarded([&] {
+    if (plans < 0) throw std::invalid_argument("plan cache capacity must be >= 0");
+    std::lock_guard<std::mutex> lock(g_cacheMutex);
+    g_cacheCapacity = plans;
+    evictLocked();
+  });
+}
+
+int fkt_plan_cache_size(void) {
+  std::lock_guard<std::mutex> lock(g_cacheMutex);
+  return static_cast<int>(g_cache.size());
 }
 
 int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info) {
