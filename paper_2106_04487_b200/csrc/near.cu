@@ -23,6 +23,10 @@ constexpr int kNearThreads = 128;
 constexpr int kNearTPT = 2;
 constexpr int kNearChunk = 512;  // sources staged per pass (generic kernel)
 constexpr int kFastChunk = 512;  // sources staged per pass (fast kernel)
+// CTAs/SM hint per kernel (B200 sweep, 64-thread CTAs): Matern-3/2 in 3-D runs
+// fastest capped at 10 CTAs (<= 102 registers; cfg2 K3 13.61 -> 13.42 ms);
+// the others are best left to ptxas (cfg3/cfg4 slower when capped).
+constexpr int nearMinBlocks(int kid, int d) { return kid == FKTB_KERNEL_MATERN32 && d == 3 ? 10 : 1; }
 
 struct NearArgs {
   int n, d, nrhs;
@@ -121,7 +125,7 @@ struct FastArgs {
 // right-hand sides per pass (the kernel value is evaluated once per pair and
 // reused for all R weights).
 template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
-__global__ void __launch_bounds__(THREADS) near_fast(const __grid_constant__ FastArgs F) {
+__global__ void __launch_bounds__(THREADS, (THREADS == 64 ? nearMinBlocks(KID, D) : 1)) near_fast(const __grid_constant__ FastArgs F) {
   static_assert(THREADS * TPT == kNearThreads * kNearTPT, "near tile size");
   constexpr int SP = (D + R + 1) / 2 * 2;  // AoS stride (coords + R weights), even
   constexpr int CHUNK = R > 2 ? 256 : kFastChunk;

@@ -1,4 +1,1 @@
-timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-mkdir -p gpurun_out
-bash scripts/gpu_bench_all.sh
-python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 400 gpurun_out/bench_default.json
+for c in 2 3 4; do echo "cfg$c $(SWEEP_CFG=$c python scripts/sweep_near.py 0)"; done
