@@ -196,7 +196,7 @@ void buildTiles(DevicePlan& plan) {
 }
 
 void clearGraphs(DevicePlan& plan) {
-  for (auto& kv : plan.graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : plan.graphs) cudaGraphExecDestroy(kv.second.first);
   plan.graphs.clear();
 }
 
@@ -469,9 +469,20 @@ void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cuda
     const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     FKTB_CUDA(e);
-    it = plan.graphs.emplace(key, exec).first;
+    if (static_cast<int>(plan.graphs.size()) >= DevicePlan::kMaxGraphs) {
+      auto victim = plan.graphs.begin();
+      for (auto g = plan.graphs.begin(); g != plan.graphs.end(); ++g)
+        if (g->second.second < victim->second.second) victim = g;
+      // the victim may still be in flight on a stream the caller owns (or
+      // has destroyed): drain the device before releasing it (rare path)
+      FKTB_CUDA(cudaDeviceSynchronize());
+      cudaGraphExecDestroy(victim->second.first);
+      plan.graphs.erase(victim);
+    }
+    it = plan.graphs.emplace(key, std::make_pair(exec, 0ull)).first;
   }
-  FKTB_CUDA(cudaGraphLaunch(it->second, st));
+  it->second.second = ++plan.graphClock;
+  FKTB_CUDA(cudaGraphLaunch(it->second.first, st));
 }
 
 }  // namespace fktb

@@ -168,7 +168,13 @@ struct DevicePlan {
   DeviceBuffer<double> dCom;
   // Captured CUDA graphs of the whole MVM, per (y, z, nrhs, stream); replayed
   // on repeat calls (launch-bound small problems). Cleared on reallocation.
-  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, cudaGraphExec_t> graphs;
+  // Bounded: callers that pass fresh buffers every call would otherwise grow
+  // it without limit; the least recently launched graph is dropped past
+  // kMaxGraphs.
+  static constexpr int kMaxGraphs = 8;
+  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, std::pair<cudaGraphExec_t, unsigned long long>>
+      graphs;
+  unsigned long long graphClock = 0;
   bool useGraphs = true;
 };
 
