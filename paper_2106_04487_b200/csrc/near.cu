@@ -125,7 +125,7 @@ struct FastArgs {
 // right-hand sides per pass (the kernel value is evaluated once per pair and
 // reused for all R weights).
 template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
-__global__ void __launch_bounds__(THREADS, (THREADS == 64 ? nearMinBlocks(KID, D) : 1)) near_fast(const __grid_constant__ FastArgs F) {
+__global__ void __launch_bounds__(THREADS, (THREADS == 64 && R == 1 ? nearMinBlocks(KID, D) : 1)) near_fast(const __grid_constant__ FastArgs F) {
   static_assert(THREADS * TPT == kNearThreads * kNearTPT, "near tile size");
   constexpr int SP = (D + R + 1) / 2 * 2;  // AoS stride (coords + R weights), even
   constexpr int CHUNK = R > 2 ? 256 : kFastChunk;
@@ -229,7 +229,16 @@ void launchFastSel(const FastArgs& F, int nrhs, int tiles, cudaStream_t st) {
     }
     return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, st);
   }
-  if (nrhs % 16 == 0) return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, st);
+  if (nrhs % 16 == 0) {
+    // 4 targets x 16 RHS accumulators per thread: each source's 16 weights
+    // (8 LDS.128) serve 64 FMAs (cfg5 K3 4.95 -> 4.21 ms vs 1 target/thread)
+    switch (nearVariant()) {  // tuning knob (cfg5 shapes)
+      case 11: return launchFastV<KID, D, SEL, 128, 2, 2, 16>(F, tiles, st);
+      case 14: return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, st);
+      default: break;
+    }
+    return launchFastV<KID, D, SEL, 64, 4, 1, 16>(F, tiles, st);
+  }
   if (nrhs % 8 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 8>(F, tiles, st);
   if (nrhs % 4 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 4>(F, tiles, st);
   if (nrhs % 2 == 0) return launchFastV<KID, D, SEL, 64, 4, 2, 2>(F, tiles, st);
