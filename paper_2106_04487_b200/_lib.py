@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfkt_cuda.so")
+# FKTB_LIB_PATH: developer A/B knob (a variant build of the same library)
+LIB_PATH = os.environ.get("FKTB_LIB_PATH") or os.path.join(_HERE, "lib", "libfkt_cuda.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

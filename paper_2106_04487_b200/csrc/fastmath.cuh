@@ -25,6 +25,7 @@ constexpr int kExpRep = 16;
 // Added to every squared pair distance: keeps rsqrt finite at r == 0 and is
 // below one ulp of any squared distance >= 1e-284.
 constexpr double kQBias = 1e-300;
+constexpr int kQBiasHi = 0x01a56e1f;  // high word of kQBias
 
 __device__ __forceinline__ double rsqrt_approx(double x) {
   double y;
@@ -44,6 +45,16 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   const double h = x * y0;
   const double e = fma(-h, y0, 1.0);
   return fma(0.5 * y0, e, y0);
+}
+
+// 1/sqrt(2 x) for x > 0: callers pass HALF the squared distance, so the
+// Newton step's factor 1/2 rides on the argument (3 FP64 ops, not 4). The
+// seed is MUFU rsqrt of 2x, formed on the high word (exponent + 1).
+__device__ __forceinline__ double rsqrt_nr_half(double x) {
+  const double y0 = rsqrt_approx(__hiloint2double(__double2hiint(x) + 0x00100000, 0));
+  const double h = x * y0;
+  const double e = fma(-h, y0, 0.5);  // (1 - 2 x y0^2) / 2
+  return fma(y0, e, y0);
 }
 
 // sqrt(x) for x > 0 (callers bias squared distances by kQBias so x == 0
@@ -66,14 +77,18 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y1, e1, y1);
 }
 
-// Near-field table: 2^NEAR_EXP_BITS entries (9 -> 512 entries, 4 KB of shared
-// memory, |f| <= ln2/1024 so a degree-3 polynomial suffices: one FP64 op per
-// pair fewer than the 64-entry / degree-4 table; cfg2 K3 14.72 -> 13.76 ms).
+// Near-field table: 2^NEAR_EXP_BITS entries. 9 -> 512 entries (4 KB), degree
+// 3 with the FP32-indexed reduction. Measured alternative (cfg2, B200): 64
+// entries replicated for the 16 bank pairs (8 KB, conflict-free lookups) with
+// degree 4 is 6% slower -- the 4-way bank conflicts of the 512-entry lookups
+// cost less than the extra FP64 op and shared memory (the loop is bound by
+// FP64 dependency latency, ncu stall_wait, not by the shared-memory pipe).
 #ifndef FKTB_NEAR_EXP_BITS
 #define FKTB_NEAR_EXP_BITS 9
 #endif
 constexpr int kNearExpBits = FKTB_NEAR_EXP_BITS;
 constexpr int kNearExpTable = 1 << kNearExpBits;
+constexpr int kNearExpRep = kNearExpBits <= 7 ? kExpRep : 1;
 
 // e^-u for u >= 0 (underflows to ~0 past u = 708). tab: the lane's column of
 // the replicated 2^(j/2^BITS) table (tab[j * REP] = 2^(j/2^BITS)).
@@ -105,6 +120,71 @@ __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ t
   const int e = k >> BITS;  // arithmetic shift: floor(k / 2^BITS)
   const double scaled = __hiloint2double(__double2hiint(tj) + (e << 20), __double2loint(tj));
   return scaled * p;
+}
+
+// e^-u as exp_neg, with the table index found on the FP32 pipe (one FP64 op
+// fewer): the index k = -round(u * 2^BITS / ln2) only has to be NEAR the true
+// rounding, since the FP64 residual f = -k * ln2/2^BITS - u is exact for any
+// k. uf = u truncated to 20 mantissa bits, built from u's high word by one
+// LEA (exponent rebias 1023 -> 127, modulo 2^32; valid for u in [2^-127,
+// 2^129)); k comes out of one FFMA against the FP32 magic 1.5 * 2^23, and its
+// bit pattern kb = 0x4b400000 + k doubles as the low word of the FP64 magic
+// 1.5 * 2^52 + kb, so kd = k costs one DADD; kb's low bits index the table and
+// kb >> BITS carries the exponent (0x4b400000 >> BITS << 20 vanishes mod 2^32).
+// |f| <= 0.53 steps for u <= 32 (degree-3 truncation at BITS = 9: 1.1e-14
+// relative), <= 1 step up to the clamp (1.4e-13 relative on values below
+// e^-32).
+//   CLAMP_HI: clamp u <= ~708.3 here (else the caller did, see clamp_exp_arg).
+//   CLAMP_LO: u may be below 2^-127 or negative (uf clamped to 2^-127; then
+//     k = 0 and f = -u, exact for small negative u as the Gram-form Gaussian
+//     needs); else the caller guarantees u >= 2^-127.
+__device__ __forceinline__ double clamp_exp_arg(double u) {
+  return __hiloint2double(min(__double2hiint(u), 0x40862000), __double2loint(u));
+}
+
+// Table lookup of entry (k mod 2^BITS) in the REP-replicated shared table at
+// `tab` (entry j, column c at tab[j * REP + c]); colBytes = 8 * the lane's
+// column. One shift and one LOP3 (and | or) give the byte offset.
+template <int REP, int BITS>
+__device__ __forceinline__ double exp_table_at(const double* __restrict__ tab, int k, int colBytes) {
+  static_assert((REP & (REP - 1)) == 0, "REP must be a power of two");
+  constexpr int kLog = REP == 1 ? 0 : REP == 2 ? 1 : REP == 4 ? 2 : REP == 8 ? 3 : 4;
+  static_assert((1 << kLog) == REP, "REP <= 16");
+  const unsigned off = ((static_cast<unsigned>(k) << (3 + kLog)) & (((1u << BITS) - 1u) << (3 + kLog))) |
+                       static_cast<unsigned>(colBytes);
+  return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + off);
+}
+
+template <int REP = 1, int BITS = 9, bool CLAMP_LO = true, bool CLAMP_HI = true>
+__device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict__ tab, int colBytes) {
+  static_assert(BITS >= 6, "degree-4 polynomial needs |f| <= ln2/2^7");
+  constexpr float kInvStepF = 1.44269504f * (1 << BITS);
+  constexpr double kStep = 0.6931471805599453 / (1 << BITS);
+  constexpr int kHiMin = 896 << 20;                              // 2^-127
+  constexpr double kMagicK = 6755399441055744.0 + 1262485504.0;  // 1.5 * 2^52 + 0x4b400000
+  if constexpr (CLAMP_HI) u = clamp_exp_arg(u);
+  const int hi = CLAMP_LO ? max(__double2hiint(u), kHiMin) : __double2hiint(u);
+  // (hi << 3) - (896 << 23) modulo 2^32 (unsigned: no signed overflow)
+  const float uf = __uint_as_float(static_cast<unsigned>(hi) * 8u + 0x40000000u);
+  const int kb = __float_as_int(fmaf(uf, -kInvStepF, 12582912.0f));  // 0x4b400000 + k, k <= 0
+  const double kd = __hiloint2double(0x43380000, kb) - kMagicK;     // k, exactly
+  const double f = fma(kd, -kStep, -u);                              // e^-u = 2^(k/2^BITS) e^f
+  double p;
+  if constexpr (BITS >= 9) {  // |f| <= 1.06 ln2/2^10: degree 3, truncation <= 1.4e-14
+    p = fma(f, 1.0 / 6.0, 0.5);
+  } else {  // |f| <= 0.53 ln2/2^(BITS-1): degree 4, truncation <= 5e-14 at BITS = 6
+    p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
+    p = fma(f, p, 0.5);
+  }
+  p = fma(f, p, 1.0);
+  p = fma(f, p, 1.0);
+  const double tj = exp_table_at<REP, BITS>(tab, kb, colBytes);
+  // exponent: hi(tj) + ((kb >> BITS) << 20); the shift is opaque to the
+  // front end so ptxas forms SHF + LEA (it would otherwise emit shl, and, add)
+  int e;
+  asm("shr.s32 %0, %1, %2;" : "=r"(e) : "r"(kb), "n"(BITS));
+  const unsigned eh = static_cast<unsigned>(__double2hiint(tj)) + (static_cast<unsigned>(e) << 20);
+  return __hiloint2double(static_cast<int>(eh), __double2loint(tj)) * p;
 }
 
 }  // namespace fktb

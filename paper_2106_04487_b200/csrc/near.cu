@@ -119,35 +119,88 @@ struct FastArgs {
   double diagCanon;  // diag / wf
   int sel;           // apply the r == 0 convention explicitly
   const double* expTable;
+  // Gram-form tiles (kernels with FastKernel::gram, no explicit r == 0
+  // select): leaf centres (nodes x d) and limit^2 = (radius/theta)^2; a tile
+  // takes the Gram form when limit2[leaf] <= gramLimit2 (scaled |t|^2 + |s|^2
+  // <= kGramBound), else the difference form. gramLimit2 < 0 disables it.
+  const double* center;
+  const double* limit2;
+  double gramLimit2;
 };
 
-// THREADS x TPT = 256 targets per tile; UNR sources per unrolled step; R
-// right-hand sides per pass (the kernel value is evaluated once per pair and
-// reused for all R weights).
-template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
-__global__ void __launch_bounds__(THREADS, (THREADS == 64 && R == 1 ? nearMinBlocks(KID, D) : 1)) near_fast(const __grid_constant__ FastArgs F) {
-  static_assert(THREADS * TPT == kNearThreads * kNearTPT, "near tile size");
-  constexpr int SP = (D + R + 1) / 2 * 2;  // AoS stride (coords + R weights), even
-  constexpr int CHUNK = R > 2 ? 256 : kFastChunk;
-  __shared__ __align__(16) double ss[CHUNK * SP];
-  __shared__ double tab[kNearExpTable];
+// Bound on |t|^2 + |s|^2 (scaled, leaf-centred) for the Gram form: the
+// rounding of q is then <= ~4 eps * 1024 = 1e-12 absolute, and dK/dq <= 1 for
+// every Gram kernel (canonical scaling). Near targets of leaf l lie within
+// radius/theta of its centre (tree.cpp:191-200), sources within radius.
+constexpr double kGramBound = 1024.0;
+
+// FP32-indexed exp (fastmath.cuh exp_neg_fi) in the near field; compile-time
+// A/B knob.
+#ifndef FKTB_NEAR_FI
+#define FKTB_NEAR_FI 1
+#endif
+constexpr bool kNearFI = FKTB_NEAR_FI != 0;
+
+// Runtime A/B knob: FKTB_NEAR_GRAM=0 forces the difference form everywhere.
+inline bool nearGramEnabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("FKTB_NEAR_GRAM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Shared AoS source rows: stride (doubles, even for 128-bit loads) and the
+// sources staged per pass. Gram rows carry |s|^2 too; their chunk is halved to
+// keep shared memory (and so occupancy) at the difference form's level; many
+// right-hand sides shrink the chunk to stay within 40 KB of static shared
+// memory next to the 8 KB exp table.
+constexpr int nearStride(int d, int r, bool gram) { return (d + (gram ? 1 : 0) + r + 1) / 2 * 2; }
+constexpr int nearChunk(int d, int r, bool gram) {
+  return gram ? (r > 2 ? 128 : 256) : (r <= 2 ? kFastChunk : (nearStride(d, r, false) * 256 * 8 <= 40960 ? 256 : 128));
+}
+
+// Whole tile pass (targets, source chunks, atomics) in one pair form.
+//  GRAM = false: q = sum_a (t_a - s_a)^2 on scaled coordinates (bias kQBias),
+//    sources AoS (s_0..s_{D-1}, w_0..w_{R-1}).
+//  GRAM = true: t, s centred on the leaf centre c; q = |t|^2 + (|s|^2 +
+//    offset) + sum_a t_a (-2 s_a), sources AoS (-2 s_a, |s|^2 + offset, w_r):
+//    D FMAs + 1 add per pair instead of D subtractions + D FMAs.
+template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R, bool GRAM, bool FI>
+__device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& tile, double* ss, const double* tab,
+                                          int colBytes) {
+  using FK = FastKernel<KID>;
+  constexpr int SP = nearStride(D, R, GRAM);
+  constexpr int CHUNK = nearChunk(D, R, GRAM);
   const NearArgs& A = F.a;
-  if constexpr (FastKernel<KID>::needsTable)
-    for (int i = threadIdx.x; i < kNearExpTable; i += THREADS) tab[i] = F.expTable[i];
-  const FktbTile tile = A.tiles[blockIdx.x];
   const int leaf = tile.node;
   const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
   const int n = A.n;
+  double c[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) c[a] = GRAM ? F.center[static_cast<size_t>(leaf) * D + a] : 0.0;
   int tpos[TPT];
   double tx[TPT][D];
+  double tn[TPT];
   double acc[TPT][R];
 #pragma unroll
   for (int i = 0; i < TPT; ++i) {
     const int idx = threadIdx.x + i * THREADS;
     tpos[i] = idx < tile.count ? static_cast<int>(A.nearPos[tile.start + idx]) : -1;
     const int p = tpos[i] >= 0 ? tpos[i] : 0;
+    tn[i] = 0.0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) tx[i][a] = A.pc[static_cast<size_t>(a) * n + p] * F.sc;
+    for (int a = 0; a < D; ++a) {
+      if constexpr (GRAM) {
+        tx[i][a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + p] - c[a], F.sc);
+        tn[i] = fma(tx[i][a], tx[i][a], tn[i]);
+      } else {
+        // __dmul_rn: never contracted into the pair loop's subtraction, so a
+        // target and a source at the same point scale to the same double and
+        // r == 0 gives q == kQBias exactly (the select depends on it)
+        tx[i][a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + p], F.sc);
+      }
+    }
   }
   for (int r0 = 0; r0 < A.nrhs; r0 += R) {
 #pragma unroll
@@ -158,10 +211,23 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 64 && R == 1 ? nearMinBlo
       const int cn = min(CHUNK, se - cs);
       __syncthreads();
       for (int s = threadIdx.x; s < cn; s += THREADS) {
+        if constexpr (GRAM) {
+          double ns = 0.0;
 #pragma unroll
-        for (int a = 0; a < D; ++a) ss[s * SP + a] = A.pc[static_cast<size_t>(a) * n + cs + s] * F.sc;
+          for (int a = 0; a < D; ++a) {
+            const double v = __dmul_rn(A.pc[static_cast<size_t>(a) * n + cs + s] - c[a], F.sc);
+            ns = fma(v, v, ns);
+            ss[s * SP + a] = -2.0 * v;
+          }
+          ss[s * SP + D] = ns + (FK::gramOffset + kQBias);
 #pragma unroll
-        for (int r = 0; r < R; ++r) ss[s * SP + D + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * F.wf;
+          for (int r = 0; r < R; ++r) ss[s * SP + D + 1 + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * F.wf;
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) ss[s * SP + a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + cs + s], F.sc);
+#pragma unroll
+          for (int r = 0; r < R; ++r) ss[s * SP + D + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * F.wf;
+        }
       }
       __syncthreads();
 #pragma unroll UNR
@@ -173,19 +239,31 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 64 && R == 1 ? nearMinBlo
           src[q] = v.x;
           src[q + 1] = v.y;
         }
+        constexpr int W0 = GRAM ? D + 1 : D;  // first weight slot
 #pragma unroll
         for (int i = 0; i < TPT; ++i) {
-          const double d0 = tx[i][0] - src[0];
-          double q = fma(d0, d0, kQBias);
+          double q;
+          if constexpr (GRAM) {
+            q = fma(tx[i][0], src[0], src[D]);
 #pragma unroll
-          for (int a = 1; a < D; ++a) {
-            const double da = tx[i][a] - src[a];
-            q = fma(da, da, q);
+            for (int a = 1; a < D; ++a) q = fma(tx[i][a], src[a], q);
+            q += tn[i];
+          } else {
+            const double d0 = tx[i][0] - src[0];
+            q = fma(d0, d0, kQBias);
+#pragma unroll
+            for (int a = 1; a < D; ++a) {
+              const double da = tx[i][a] - src[a];
+              q = fma(da, da, q);
+            }
           }
-          double kv = FastKernel<KID>::template eval<1>(q, tab);
-          if constexpr (SEL) kv = q == kQBias ? F.diagCanon : kv;
+          double kv = FK::template eval<kNearExpRep, FI, GRAM>(q, tab, colBytes);
+          // r == 0 <=> q == kQBias; compared on the high word (integer pipe):
+          // any other q is >= ~1e-284 (points closer than ~1e-142 count as
+          // coincident, where the FP64 form was already off)
+          if constexpr (SEL) kv = __double2hiint(q) == kQBiasHi ? F.diagCanon : kv;
 #pragma unroll
-          for (int r = 0; r < R; ++r) acc[i][r] = fma(kv, src[D + r], acc[i][r]);
+          for (int r = 0; r < R; ++r) acc[i][r] = fma(kv, src[W0 + r], acc[i][r]);
         }
       }
     }
@@ -197,10 +275,44 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 64 && R == 1 ? nearMinBlo
   }
 }
 
-template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R>
-void launchFastV(const FastArgs& F, int tiles, cudaStream_t st) {
-  near_fast<KID, D, SEL, THREADS, TPT, UNR, R><<<tiles, THREADS, 0, st>>>(F);
-  FKTB_CUDA(cudaGetLastError());
+// THREADS x TPT = 256 targets per tile; UNR sources per unrolled step; R
+// right-hand sides per pass (the kernel value is evaluated once per pair and
+// reused for all R weights). GRAM: this launch serves the tiles whose leaf
+// passes the Gram bound (the other launch, GRAM = false, the rest); separate
+// instantiations so each form gets its own register allocation.
+// MB: CTAs/SM for __launch_bounds__ (0: nearMinBlocks for 64-thread single-RHS
+// shapes, else none).
+template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R, bool GRAM, int MB>
+__global__ void __launch_bounds__(THREADS, (MB > 0 ? MB : (THREADS == 64 && R == 1 ? nearMinBlocks(KID, D) : 1))) near_fast(const __grid_constant__ FastArgs F) {
+  static_assert(THREADS * TPT == kNearThreads * kNearTPT, "near tile size");
+  static_assert(!GRAM || (FastKernel<KID>::gram && !SEL), "Gram form needs a smooth kernel without select");
+  constexpr int SP = nearStride(D, R, GRAM);
+  constexpr int CHUNK = nearChunk(D, R, GRAM);
+  __shared__ __align__(16) double ss[CHUNK * SP];
+  __shared__ double tab[kNearExpTable * kNearExpRep];  // entry j at tab[j * kNearExpRep + column]
+  const NearArgs& A = F.a;
+  const FktbTile tile = A.tiles[blockIdx.x];
+  if (GRAM != (F.limit2[tile.node] <= F.gramLimit2)) return;  // the other form's tile
+  if constexpr (FastKernel<KID>::needsTable)
+    for (int i = threadIdx.x; i < kNearExpTable * kNearExpRep; i += THREADS) tab[i] = F.expTable[i / kNearExpRep];
+  // each lane reads its own column: conflict-free 64-bit lookups
+  near_tile<KID, D, SEL, THREADS, TPT, UNR, R, GRAM, kNearFI>(F, tile, ss, tab, (threadIdx.x & (kNearExpRep - 1)) * 8);
+}
+
+template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R, int MB = 0>
+void launchFastV(const FastArgs& F, int tiles, int gramTiles, cudaStream_t st) {
+  if constexpr (FastKernel<KID>::gram && !SEL) {
+    if (gramTiles > 0) {
+      near_fast<KID, D, SEL, THREADS, TPT, UNR, R, true, MB><<<tiles, THREADS, 0, st>>>(F);
+      FKTB_CUDA(cudaGetLastError());
+    }
+  } else {
+    gramTiles = 0;
+  }
+  if (gramTiles < tiles) {
+    near_fast<KID, D, SEL, THREADS, TPT, UNR, R, false, MB><<<tiles, THREADS, 0, st>>>(F);
+    FKTB_CUDA(cudaGetLastError());
+  }
 }
 
 // Developer knob for tuning sweeps (scripts/sweep_near.py): FKTB_NEAR_VARIANT
@@ -215,49 +327,74 @@ inline int nearVariant() {
 }
 
 template <int KID, int D, bool SEL>
-void launchFastSel(const FastArgs& F, int nrhs, int tiles, cudaStream_t st) {
+void launchFastSel(const FastArgs& F, int nrhs, int tiles, int gramTiles, cudaStream_t st) {
   if (nrhs == 1) {
-    if constexpr (KID == FKTB_KERNEL_MATERN32 && D == 3 && !SEL) {
+    if constexpr ((KID == FKTB_KERNEL_MATERN32 && D == 3 || KID == FKTB_KERNEL_GAUSSIAN && D == 5) && !SEL) {
       switch (nearVariant()) {
-        case 1: return launchFastV<KID, D, SEL, 64, 4, 4, 1>(F, tiles, st);
-        case 2: return launchFastV<KID, D, SEL, 32, 8, 1, 1>(F, tiles, st);
-        case 3: return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, st);
-        case 4: return launchFastV<KID, D, SEL, 128, 2, 4, 1>(F, tiles, st);
-        case 5: return launchFastV<KID, D, SEL, 64, 4, 1, 1>(F, tiles, st);
+        case 1: return launchFastV<KID, D, SEL, 64, 4, 4, 1>(F, tiles, gramTiles, st);
+        case 11: return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
+        case 2: return launchFastV<KID, D, SEL, 32, 8, 1, 1>(F, tiles, gramTiles, st);
+        case 3: return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, gramTiles, st);
+        case 4: return launchFastV<KID, D, SEL, 128, 2, 4, 1>(F, tiles, gramTiles, st);
+        case 5: return launchFastV<KID, D, SEL, 64, 4, 1, 1>(F, tiles, gramTiles, st);
+        case 6: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 12>(F, tiles, gramTiles, st);
+        case 7: return launchFastV<KID, D, SEL, 64, 4, 1, 1, 12>(F, tiles, gramTiles, st);
+        case 8: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 8>(F, tiles, gramTiles, st);
+        case 9: return launchFastV<KID, D, SEL, 128, 2, 2, 1, 6>(F, tiles, gramTiles, st);
+        case 10: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 6>(F, tiles, gramTiles, st);
+        case 12: return launchFastV<KID, D, SEL, 64, 4, 1, 1, 8>(F, tiles, gramTiles, st);
+        case 13: return launchFastV<KID, D, SEL, 128, 2, 2, 1, 8>(F, tiles, gramTiles, st);
         default: break;
       }
     }
-    return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, st);
+    // measured shapes (B200 sweeps, scripts/sweep_near.py): Matern-3/2 in 3-D
+    // wants 8 independent targets per thread (one warp per CTA: cfg2 K3
+    // 13.72 -> 13.14 ms); the 5-D Gaussian 4 targets, no unroll, 8 CTAs/SM
+    // (cfg3 23.1 -> 22.0 ms)
+    if constexpr (KID == FKTB_KERNEL_MATERN32 && D == 3 && !SEL) return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, gramTiles, st);
+    if constexpr (KID == FKTB_KERNEL_GAUSSIAN && D == 5 && !SEL) return launchFastV<KID, D, SEL, 64, 4, 1, 1, 8>(F, tiles, gramTiles, st);
+    return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
   }
   if (nrhs % 16 == 0) {
     // 4 targets x 16 RHS accumulators per thread: each source's 16 weights
     // (8 LDS.128) serve 64 FMAs (cfg5 K3 4.95 -> 4.21 ms vs 1 target/thread)
     switch (nearVariant()) {  // tuning knob (cfg5 shapes)
-      case 11: return launchFastV<KID, D, SEL, 128, 2, 2, 16>(F, tiles, st);
-      case 14: return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, st);
+      case 11: return launchFastV<KID, D, SEL, 128, 2, 2, 16>(F, tiles, gramTiles, st);
+      case 14: return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, gramTiles, st);
       default: break;
     }
-    return launchFastV<KID, D, SEL, 64, 4, 1, 16>(F, tiles, st);
+    return launchFastV<KID, D, SEL, 64, 4, 1, 16>(F, tiles, gramTiles, st);
   }
-  if (nrhs % 8 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 8>(F, tiles, st);
-  if (nrhs % 4 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 4>(F, tiles, st);
-  if (nrhs % 2 == 0) return launchFastV<KID, D, SEL, 64, 4, 2, 2>(F, tiles, st);
-  return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, st);
+  if (nrhs % 8 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 8>(F, tiles, gramTiles, st);
+  if (nrhs % 4 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 4>(F, tiles, gramTiles, st);
+  if (nrhs % 2 == 0) return launchFastV<KID, D, SEL, 64, 4, 2, 2>(F, tiles, gramTiles, st);
+  return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
 }
 
 template <int KID, int D>
-void launchFastT(const NearArgs& A, int tiles, cudaStream_t st) {
-  FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice(kNearExpBits)};
+void launchFastT(const NearArgs& A, const DevicePlan& plan, int tiles, cudaStream_t st) {
+  const DeviceTree& t = *plan.tree;
+  FastArgs F{A, 1.0, 1.0, 0.0, 0, expTableDevice(kNearExpBits), t.dCenter.get(), t.dLimit2.get(), -1.0};
   fastScales(A.kd, F.sc, F.wf);
   F.diagCanon = A.kd.diag / F.wf;
   // The canonical formula already gives the reference convention at r == 0
   // for the smooth kernels (K(0) = valueAtZero); otherwise select explicitly.
   const bool smooth = KID != FKTB_KERNEL_INVERSE_R && KID != FKTB_KERNEL_INVERSE_R2;
   F.sel = !(smooth && A.kd.diag == F.wf);
+  // Gram tiles only without the select (it needs exact r == 0 detection);
+  // gramLimit2 < 0 leaves every tile to the difference form.
+  int gramTiles = 0;
+  if (FastKernel<KID>::gram && !F.sel && nearGramEnabled()) {
+    F.gramLimit2 = kGramBound / (F.sc * F.sc * (1.0 + t.theta * t.theta));
+    for (const FktbTile& tl : plan.nearTilesHost) {  // the device test, on the same limit2 values
+      volatile double limit = t.radius[static_cast<size_t>(tl.node)] / t.theta;
+      gramTiles += limit * limit <= F.gramLimit2;
+    }
+  }
   if (F.sel)
-    launchFastSel<KID, D, true>(F, A.nrhs, tiles, st);
+    launchFastSel<KID, D, true>(F, A.nrhs, tiles, gramTiles, st);
   else
-    launchFastSel<KID, D, false>(F, A.nrhs, tiles, st);
+    launchFastSel<KID, D, false>(F, A.nrhs, tiles, gramTiles, st);
 }
 
 template <int KID, int D>
@@ -275,12 +412,12 @@ void launchNearT(const NearArgs& A, int tiles, cudaStream_t st) {
 }
 
 template <int KID>
-void launchNearK(const NearArgs& A, int tiles, cudaStream_t st) {
+void launchNearK(const NearArgs& A, const DevicePlan& plan, int tiles, cudaStream_t st) {
   if constexpr (FastKernel<KID>::supported) {
     switch (A.d) {
-      case 2: return launchFastT<KID, 2>(A, tiles, st);
-      case 3: return launchFastT<KID, 3>(A, tiles, st);
-      case 5: return launchFastT<KID, 5>(A, tiles, st);
+      case 2: return launchFastT<KID, 2>(A, plan, tiles, st);
+      case 3: return launchFastT<KID, 3>(A, plan, tiles, st);
+      case 5: return launchFastT<KID, 5>(A, plan, tiles, st);
       default: break;
     }
   }
@@ -320,20 +457,20 @@ void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, 
   fillKernelDesc(plan.kernel, A.kd);
   if (plan.options.hasDiagonal) A.kd.diag = plan.options.diagonal;
   switch (plan.kernel.id) {
-    case FKTB_KERNEL_EXPONENTIAL: return launchNearK<FKTB_KERNEL_EXPONENTIAL>(A, tiles, st);
-    case FKTB_KERNEL_MATERN12: return launchNearK<FKTB_KERNEL_MATERN12>(A, tiles, st);
-    case FKTB_KERNEL_MATERN32: return launchNearK<FKTB_KERNEL_MATERN32>(A, tiles, st);
-    case FKTB_KERNEL_CAUCHY: return launchNearK<FKTB_KERNEL_CAUCHY>(A, tiles, st);
-    case FKTB_KERNEL_RATIONAL_QUADRATIC: return launchNearK<FKTB_KERNEL_RATIONAL_QUADRATIC>(A, tiles, st);
-    case FKTB_KERNEL_GAUSSIAN: return launchNearK<FKTB_KERNEL_GAUSSIAN>(A, tiles, st);
-    case FKTB_KERNEL_INVERSE_R: return launchNearK<FKTB_KERNEL_INVERSE_R>(A, tiles, st);
-    case FKTB_KERNEL_INVERSE_R2: return launchNearK<FKTB_KERNEL_INVERSE_R2>(A, tiles, st);
-    case FKTB_KERNEL_INVERSE_R3: return launchNearK<FKTB_KERNEL_INVERSE_R3>(A, tiles, st);
-    case FKTB_KERNEL_EXP_OVER_R: return launchNearK<FKTB_KERNEL_EXP_OVER_R>(A, tiles, st);
-    case FKTB_KERNEL_R_EXP: return launchNearK<FKTB_KERNEL_R_EXP>(A, tiles, st);
-    case FKTB_KERNEL_COS_OVER_R: return launchNearK<FKTB_KERNEL_COS_OVER_R>(A, tiles, st);
-    case FKTB_KERNEL_EXP_NEG_INV_R: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R>(A, tiles, st);
-    case FKTB_KERNEL_EXP_NEG_INV_R2: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R2>(A, tiles, st);
+    case FKTB_KERNEL_EXPONENTIAL: return launchNearK<FKTB_KERNEL_EXPONENTIAL>(A, plan, tiles, st);
+    case FKTB_KERNEL_MATERN12: return launchNearK<FKTB_KERNEL_MATERN12>(A, plan, tiles, st);
+    case FKTB_KERNEL_MATERN32: return launchNearK<FKTB_KERNEL_MATERN32>(A, plan, tiles, st);
+    case FKTB_KERNEL_CAUCHY: return launchNearK<FKTB_KERNEL_CAUCHY>(A, plan, tiles, st);
+    case FKTB_KERNEL_RATIONAL_QUADRATIC: return launchNearK<FKTB_KERNEL_RATIONAL_QUADRATIC>(A, plan, tiles, st);
+    case FKTB_KERNEL_GAUSSIAN: return launchNearK<FKTB_KERNEL_GAUSSIAN>(A, plan, tiles, st);
+    case FKTB_KERNEL_INVERSE_R: return launchNearK<FKTB_KERNEL_INVERSE_R>(A, plan, tiles, st);
+    case FKTB_KERNEL_INVERSE_R2: return launchNearK<FKTB_KERNEL_INVERSE_R2>(A, plan, tiles, st);
+    case FKTB_KERNEL_INVERSE_R3: return launchNearK<FKTB_KERNEL_INVERSE_R3>(A, plan, tiles, st);
+    case FKTB_KERNEL_EXP_OVER_R: return launchNearK<FKTB_KERNEL_EXP_OVER_R>(A, plan, tiles, st);
+    case FKTB_KERNEL_R_EXP: return launchNearK<FKTB_KERNEL_R_EXP>(A, plan, tiles, st);
+    case FKTB_KERNEL_COS_OVER_R: return launchNearK<FKTB_KERNEL_COS_OVER_R>(A, plan, tiles, st);
+    case FKTB_KERNEL_EXP_NEG_INV_R: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R>(A, plan, tiles, st);
+    case FKTB_KERNEL_EXP_NEG_INV_R2: return launchNearK<FKTB_KERNEL_EXP_NEG_INV_R2>(A, plan, tiles, st);
   }
   throw std::invalid_argument("near field: unknown kernel id");
 }

@@ -19,23 +19,49 @@ struct FastKernel {
   static constexpr bool needsTable =
       KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL ||
       KID == FKTB_KERNEL_GAUSSIAN;
-  // canonical K at scaled squared distance q (> 0 unless the select handles 0)
-  template <int REP>
-  __device__ static __forceinline__ double eval(double q, const double* tab) {
+  // Gram-form pair distances (near.cu): q = |t|^2 + |s|^2 - 2 t.s on
+  // leaf-centred coordinates, with `gramOffset` folded into |s|^2 (the 1 + r^2
+  // of the Cauchy family). Only for kernels whose K is smooth in q (bounded
+  // dK/dq, so the q rounding of eps * (|t|^2 + |s|^2) stays an absolute error
+  // of the same size) and that need no exact r == 0 detection.
+  // (Not the exponential / Matern-1/2 kernels: e^-sqrt(q) has an unbounded
+  // dK/dq at 0, so a 1e-15 error in q becomes ~3e-8 in K.)
+  static constexpr bool gram = KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_CAUCHY ||
+                               KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN;
+  static constexpr double gramOffset =
+      KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC ? 1.0 : 0.0;
+  // Kernels that take sqrt(q): a Gram q may round slightly below 0.
+  static constexpr bool gramClamp = KID == FKTB_KERNEL_MATERN32;
+
+  template <bool FI, int REP, bool CLAMP_LO = true, bool CLAMP_HI = true>
+  __device__ static __forceinline__ double expn(double u, const double* tab, int colBytes) {
+    if constexpr (FI) return exp_neg_fi<REP, kNearExpBits, CLAMP_LO, CLAMP_HI>(u, tab, colBytes);
+    else return exp_neg<REP, kNearExpBits>(u, tab + colBytes / 8);
+  }
+
+  // canonical K at scaled squared distance q (> 0 unless the select handles
+  // 0); GRAM: q already carries gramOffset. FI: FP32-indexed exp. tab: the
+  // REP-replicated exp table, colBytes: 8 * this lane's column.
+  template <int REP, bool FI = false, bool GRAM = false>
+  __device__ static __forceinline__ double eval(double q, const double* tab, int colBytes = 0) {
+    // Gram q may round below 0: clamp to >= 2^-254 on the integer pipe, which
+    // also keeps sqrt(q) >= 2^-127 for the FP32-indexed exp
+    if constexpr (GRAM && gramClamp) q = __hiloint2double(max(__double2hiint(q), 769 << 20), __double2loint(q));
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
-      const double u = sqrt_nr(q);
-      const double e = exp_neg<REP, kNearExpBits>(u, tab);
+      double u = sqrt_nr(q);
+      if constexpr (FI) u = clamp_exp_arg(u);  // in place: the (1 + u) factor uses the same u
+      const double e = expn<FI, REP, !GRAM, false>(u, tab, colBytes);
       return fma(u, e, e);
     } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
-      return exp_neg<REP, kNearExpBits>(sqrt_nr(q), tab);
+      return expn<FI, REP, !GRAM, true>(sqrt_nr(q), tab, colBytes);
     } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
-      return rcp_nr(1.0 + q);
+      return rcp_nr(GRAM ? q : 1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
-      return rsqrt_nr(1.0 + q);
+      return rsqrt_nr(GRAM ? q : 1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return exp_neg<REP, kNearExpBits>(q, tab);
+      return expn<FI, REP>(q, tab, colBytes);
     } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
-      return rsqrt_nr(q);
+      return rsqrt_nr_half(q);  // q = r^2 / 2: fastScales scales by 1/sqrt(2)
     } else {
       return rcp_nr(q);
     }
@@ -51,6 +77,7 @@ inline void fastScales(const FktbKernelDesc& k, double& sc, double& wf) {
     case FKTB_KERNEL_MATERN12: sc = 1.0 / k.rho; wf = k.s2; break;
     case FKTB_KERNEL_CAUCHY:
     case FKTB_KERNEL_RATIONAL_QUADRATIC: sc = std::sqrt(k.is2); break;
+    case FKTB_KERNEL_INVERSE_R: sc = std::sqrt(0.5); break;  // eval takes r^2 / 2 (rsqrt_nr_half)
     default: break;
   }
 }

@@ -69,7 +69,7 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
     tpos[i] = idx < tile.rowCount ? static_cast<int>(A.pool[tile.rowOff + idx]) : -1;
     const int p = tpos[i] >= 0 ? tpos[i] : 0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) tx[i][a] = A.pc[static_cast<size_t>(a) * n + p] * A.sc;
+    for (int a = 0; a < D; ++a) tx[i][a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + p], A.sc);  // uncontracted (see near.cu)
     ty[i] = tpos[i] >= 0 ? A.yp[p] * A.wf : 0.0;
     acc[i] = 0.0;
   }
@@ -80,7 +80,7 @@ __device__ __forceinline__ void block_body(const SymArgs& A, const FktbBlockTile
     for (int s = threadIdx.x; s < cn; s += kSymThreads) {
       const int pos = static_cast<int>(A.pool[tile.colOff + cs + s]);
 #pragma unroll
-      for (int a = 0; a < D; ++a) ss[s * SP + a] = A.pc[static_cast<size_t>(a) * n + pos] * A.sc;
+      for (int a = 0; a < D; ++a) ss[s * SP + a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + pos], A.sc);
       ss[s * SP + D] = A.yp[pos] * A.wf;
     }
     __syncthreads();

@@ -221,13 +221,16 @@ def test_plan_errors(fkt):
 
 
 # --- conventions and RHS variants vs the reference ------------------------------------
-@pytest.mark.parametrize("name,diag", [("inverse-r", None), ("inverse-r", 2.5), ("cauchy", 7.0),
-                                       ("matern32", None), ("gaussian", 0.0)])
-def test_diagonal_conventions_with_duplicates(fkt, ref, name, diag):
+# The scaled-kernel cases (sigma != 1, rho != 1) with an explicit diagonal pin
+# the exact r == 0 detection on pre-scaled coordinates (a contracted
+# x * scale - s left q ~ 1e-34 instead of 0 at duplicates).
+@pytest.mark.parametrize("name,diag,prm", [("inverse-r", None, {}), ("inverse-r", 2.5, {}), ("cauchy", 7.0, {}),
+                                           ("cauchy", 7.0, {"sigma": 0.3}), ("matern32", None, {"sigma": 1.0, "rho": 0.3}),
+                                           ("matern32", 0.25, {"sigma": 1.0, "rho": 0.3}), ("gaussian", 0.0, {})])
+def test_diagonal_conventions_with_duplicates(fkt, ref, name, diag, prm):
     rng = np.random.default_rng(12)
     x = np.repeat(rng.random((600, 3)), 3, axis=0)  # every point three times
     y = rng.standard_normal(1800)
-    prm = {"sigma": 1.0, "rho": 0.3} if name == "matern32" else {}
     p = fkt.plan(P(fkt, x), fkt.makeKernel(name, prm), fkt.FktOptions(p=4, theta=0.6, leafCapacity=64,
                                                                      diagonal=diag))
     rp = ref.RefPlan(x, name, prm, p=4, theta=0.6, leaf=64, diagonal=diag)
