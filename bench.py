@@ -155,13 +155,21 @@ def golden_parity(cfg, z):
     return out
 
 
-def traffic_for(cfg):
+def near_ncu(cfg):
+    """ncu evidence for the near kernel at this config (profiles/near_traffic.json):
+    {"traffic": dram read + write bytes per launch, "fp64_pipe_frac": ...} or None."""
     path = os.path.join(ROOT, "profiles", "near_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(f"cfg{cfg}")
+            v = json.load(f).get(f"cfg{cfg}")
     except Exception:
         return None
+    return {"traffic": v} if isinstance(v, (int, float)) else v
+
+
+def traffic_for(cfg):
+    v = near_ncu(cfg)
+    return None if v is None else v.get("traffic")
 
 
 # ---------------------------------------------------------------------------
@@ -336,6 +344,11 @@ def run_ours(args):
             "flops_per_launch": near_flops,
             "flops_per_pair": fpp,
             "whole_step_frac": (nev_all * fpp + far_flops) / mvm_s / 1e12 / peak_tf / world,
+            # frac counts SURVEY §8(d)'s flop convention (exp = 20, sqrt / div = 8);
+            # the fast-math pair body executes fewer FP64 instructions (16 for the
+            # Matern-3/2 Gram form), so the FP64 pipe utilisation ncu measured for
+            # this kernel (profiles/near_traffic.json) is the hardware-side figure
+            "ncu_fp64_pipe_frac": (near_ncu(args.cfg) or {}).get("fp64_pipe_frac"),
         },
         "e2e": {"value": 1.0 / e2e_s, "unit": "MVM/s", "h2d_bytes_per_step": int(yh.numel() * 8) * world,
                 "d2h_bytes_per_step": int(zh.numel() * 8) * world,
