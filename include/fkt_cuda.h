@@ -127,6 +127,10 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
 int fkt_plan_set_shard(fkt_plan_t plan, int shard, int shards);
 int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi);
 int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_per_rhs);
+/* Near-field tiles (leaf, <= 256 targets) of the FP64 near field, and how many
+ * of them run the Gram pair form (leaf-centred |t|^2 + |s|^2 - 2 t.s; DESIGN.md
+ * §3) instead of the difference form. No reference counterpart (diagnostic). */
+int fkt_plan_near_forms(fkt_plan_t plan, long long* gram_tiles, long long* total_tiles);
 /* How many of this library's kernels one multiply with nrhs right-hand sides
  * launches on the current shard (memsets excluded); -1 on error. */
 long long fkt_plan_kernel_launches(fkt_plan_t plan, int nrhs);

@@ -460,6 +460,16 @@ class FktPlan:
                                          C.c_void_p(z.data_ptr() if z is not None else 0), nrhs,
                                          C.c_void_p(st.cuda_stream)))
 
+    def near_forms(self):
+        """(Gram-form tiles, all near tiles) of the FP64 near field."""
+        g, t = C.c_longlong(), C.c_longlong()
+        _check(lib.fkt_plan_near_forms(self._h, C.byref(g), C.byref(t)))
+        return int(g.value), int(t.value)
+
+    def kernel_launches(self, nrhs: int = 1) -> int:
+        """This library's kernels one multiply launches (memsets excluded)."""
+        return int(lib.fkt_plan_kernel_launches(self._h, int(nrhs)))
+
     # ---- multi-GPU target sharding (SURVEY §8e; see distributed.py) ----------
     def set_shard(self, shard: int, shards: int) -> None:
         """Own the cost-balanced, leaf-aligned target range `shard` of `shards`."""

@@ -114,6 +114,7 @@ SIGNATURES = {
     "fkt_gp_posterior_mean": (C.c_int, C.c_int, C.c_int, _d, _d, _d, C.c_char_p, _cstrs, _d, C.c_int, C.c_int, _d,
                               C.POINTER(FktGpOptionsC), _d, C.POINTER(FktCgDiagnosticsC)),
     "fkt_plan_kernel_launches": (C.c_longlong, C.c_void_p, C.c_int),
+    "fkt_plan_near_forms": (C.c_int, C.c_void_p, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)),
     "fkt_shard_cuts": (C.c_int, _u32, C.POINTER(C.c_ulonglong), C.c_int, C.c_int, C.c_uint32, _u32),
     "fkt_plan_tree": (C.c_void_p, C.c_void_p),
     "fkt_tree_create": (C.c_int, C.c_int, C.c_int, _d, C.c_int, C.POINTER(C.c_void_p)),

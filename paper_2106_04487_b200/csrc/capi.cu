@@ -524,6 +524,14 @@ int fkt_gp_posterior_mean(int n_train, int d, const double* train_x, const doubl
   });
 }
 
+int fkt_plan_near_forms(fkt_plan_t plan, long long* gram_tiles, long long* total_tiles) {
+  return guarded([&] {
+    if (!plan || !gram_tiles || !total_tiles) throw std::invalid_argument("null argument");
+    *gram_tiles = fktb::nearGramTiles(*plan->plan);
+    *total_tiles = static_cast<long long>(plan->plan->nearTilesHost.size());
+  });
+}
+
 long long fkt_plan_kernel_launches(fkt_plan_t plan, int nrhs) {
   long long out = -1;
   guarded([&] { out = fktb::kernelLaunches(*plan->plan, std::max(1, nrhs)); });

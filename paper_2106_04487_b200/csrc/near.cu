@@ -128,11 +128,14 @@ struct FastArgs {
   double gramLimit2;
 };
 
-// Bound on |t|^2 + |s|^2 (scaled, leaf-centred) for the Gram form: the
-// rounding of q is then <= ~4 eps * 1024 = 1e-12 absolute, and dK/dq <= 1 for
-// every Gram kernel (canonical scaling). Near targets of leaf l lie within
-// radius/theta of its centre (tree.cpp:191-200), sources within radius.
-constexpr double kGramBound = 1024.0;
+// Bound B on |t|^2 + |s|^2 (scaled, leaf-centred) for the Gram form. Near
+// targets of leaf l lie within radius/theta of its centre (tree.cpp:191-200),
+// sources within radius, so a tile's B = limit2 * sc^2 * (1 + theta^2). The
+// rounding of q is <= ~(4 + d) eps * B absolute (random-walk typical); every
+// Gram kernel has |dK/dq| <= 1 in canonical scaling, so K errs by <= ~1e-13
+// at B = 128 (cfg2's leaves: B ~ 7). q <= 2B keeps sqrt(q) and the Gaussian's
+// exp argument far below the exp clamp (no clamp in the pair body).
+constexpr double kGramBound = 128.0;
 
 // FP32-indexed exp (fastmath.cuh exp_neg_fi) in the near field; compile-time
 // A/B knob.
@@ -179,6 +182,15 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
   double c[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) c[a] = GRAM ? F.center[static_cast<size_t>(leaf) * D + a] : 0.0;
+  const double wf = GRAM ? F.wf * FK::gramWeight : F.wf;  // weight prefactor of this form
+  // Matern's Gram bias: q's rounding is <= (1.5 d + 0.5) eps B for this tile's
+  // B = limit2 * kGramBound / gramLimit2 (|t|^2, |s|^2: d/2 eps B each; d FMAs
+  // and one add: (d + 1)/2 eps B), so q + (1.5 d + 1) eps B + 1e-30 >= 1e-30
+  // without a clamp; it shifts K by <= half of it (|dK/dq| <= 1/2): ~3e-15 at
+  // cfg2's B ~ 7, 5e-14 at B = 70
+  const double qbias = GRAM && FK::gramBiased
+                           ? fma((1.5 * D + 1.0) * 2.220446049250313e-16 * kGramBound / F.gramLimit2, F.limit2[leaf], 1e-30)
+                           : 0.0;
   int tpos[TPT];
   double tx[TPT][D];
   double tn[TPT];
@@ -219,9 +231,9 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
             ns = fma(v, v, ns);
             ss[s * SP + a] = -2.0 * v;
           }
-          ss[s * SP + D] = ns + (FK::gramOffset + kQBias);
+          ss[s * SP + D] = ns + (FK::gramOffset + qbias);
 #pragma unroll
-          for (int r = 0; r < R; ++r) ss[s * SP + D + 1 + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * F.wf;
+          for (int r = 0; r < R; ++r) ss[s * SP + D + 1 + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * wf;
         } else {
 #pragma unroll
           for (int a = 0; a < D; ++a) ss[s * SP + a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + cs + s], F.sc);
@@ -349,10 +361,10 @@ void launchFastSel(const FastArgs& F, int nrhs, int tiles, int gramTiles, cudaSt
     }
     // measured shapes (B200 sweeps, scripts/sweep_near.py): Matern-3/2 in 3-D
     // wants 8 independent targets per thread (one warp per CTA: cfg2 K3
-    // 13.72 -> 13.14 ms); the 5-D Gaussian 4 targets, no unroll, 8 CTAs/SM
-    // (cfg3 23.1 -> 22.0 ms)
+    // 13.72 -> 13.14 ms before the clamp-free Gram form, tied with 64 x 4
+    // after it); the 5-D Gaussian 8 CTAs/SM (cfg3 22.6 -> 21.7 ms)
     if constexpr (KID == FKTB_KERNEL_MATERN32 && D == 3 && !SEL) return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, gramTiles, st);
-    if constexpr (KID == FKTB_KERNEL_GAUSSIAN && D == 5 && !SEL) return launchFastV<KID, D, SEL, 64, 4, 1, 1, 8>(F, tiles, gramTiles, st);
+    if constexpr (KID == FKTB_KERNEL_GAUSSIAN && D == 5 && !SEL) return launchFastV<KID, D, SEL, 64, 4, 2, 1, 8>(F, tiles, gramTiles, st);
     return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
   }
   if (nrhs % 16 == 0) {
@@ -371,6 +383,18 @@ void launchFastSel(const FastArgs& F, int nrhs, int tiles, int gramTiles, cudaSt
   return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
 }
 
+// Tiles whose leaf passes the Gram bound: the device test, on the same limit2
+// values (tree.cu computes limit2 the same way).
+long long countGramTiles(const DevicePlan& plan, double gramLimit2) {
+  const DeviceTree& t = *plan.tree;
+  long long g = 0;
+  for (const FktbTile& tl : plan.nearTilesHost) {
+    volatile double limit = t.radius[static_cast<size_t>(tl.node)] / t.theta;
+    g += limit * limit <= gramLimit2;
+  }
+  return g;
+}
+
 template <int KID, int D>
 void launchFastT(const NearArgs& A, const DevicePlan& plan, int tiles, cudaStream_t st) {
   const DeviceTree& t = *plan.tree;
@@ -386,10 +410,7 @@ void launchFastT(const NearArgs& A, const DevicePlan& plan, int tiles, cudaStrea
   int gramTiles = 0;
   if (FastKernel<KID>::gram && !F.sel && nearGramEnabled()) {
     F.gramLimit2 = kGramBound / (F.sc * F.sc * (1.0 + t.theta * t.theta));
-    for (const FktbTile& tl : plan.nearTilesHost) {  // the device test, on the same limit2 values
-      volatile double limit = t.radius[static_cast<size_t>(tl.node)] / t.theta;
-      gramTiles += limit * limit <= F.gramLimit2;
-    }
+    gramTiles = static_cast<int>(countGramTiles(plan, F.gramLimit2));
   }
   if (F.sel)
     launchFastSel<KID, D, true>(F, A.nrhs, tiles, gramTiles, st);
@@ -448,6 +469,26 @@ const double* expTableDevice(int bits) {
 }
 
 int nearTileSize() { return kNearThreads * kNearTPT; }
+
+// Gram-form tiles of the FP64 near_fast launch (0 when the plan's kernel,
+// dimension or diagonal convention keeps the difference form); mirrors the
+// decisions of launchFastT.
+long long nearGramTiles(const DevicePlan& plan) {
+  const int d = plan.tree->d;
+  if (d != 2 && d != 3 && d != 5) return 0;
+  const int id = plan.kernel.id;
+  const bool gram = id == FKTB_KERNEL_MATERN32 || id == FKTB_KERNEL_CAUCHY || id == FKTB_KERNEL_RATIONAL_QUADRATIC ||
+                    id == FKTB_KERNEL_GAUSSIAN;
+  if (!gram || !nearGramEnabled()) return 0;
+  FktbKernelDesc kd;
+  fillKernelDesc(plan.kernel, kd);
+  if (plan.options.hasDiagonal) kd.diag = plan.options.diagonal;
+  double sc, wf;
+  fastScales(kd, sc, wf);
+  if (kd.diag != wf) return 0;  // explicit r == 0 select
+  const DeviceTree& t = *plan.tree;
+  return countGramTiles(plan, kGramBound / (sc * sc * (1.0 + t.theta * t.theta)));
+}
 
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
   const int tiles = static_cast<int>(plan.nearTilesHost.size());

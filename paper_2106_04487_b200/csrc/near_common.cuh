@@ -28,10 +28,13 @@ struct FastKernel {
   // dK/dq at 0, so a 1e-15 error in q becomes ~3e-8 in K.)
   static constexpr bool gram = KID == FKTB_KERNEL_MATERN32 || KID == FKTB_KERNEL_CAUCHY ||
                                KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN;
+  // The Gaussian's offset 1 keeps its exp argument q + 1 >= ~1 (q may round
+  // below 0) and the factor e rides on the weights: e^-q = e * e^-(q + 1).
   static constexpr double gramOffset =
-      KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC ? 1.0 : 0.0;
-  // Kernels that take sqrt(q): a Gram q may round slightly below 0.
-  static constexpr bool gramClamp = KID == FKTB_KERNEL_MATERN32;
+      KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN ? 1.0 : 0.0;
+  static constexpr double gramWeight = KID == FKTB_KERNEL_GAUSSIAN ? 2.718281828459045 : 1.0;
+  // Matern-3/2 takes sqrt(q): its Gram q gets an additive bias (near.cu).
+  static constexpr bool gramBiased = KID == FKTB_KERNEL_MATERN32;
 
   template <bool FI, int REP, bool CLAMP_LO = true, bool CLAMP_HI = true>
   __device__ static __forceinline__ double expn(double u, const double* tab, int colBytes) {
@@ -44,12 +47,13 @@ struct FastKernel {
   // REP-replicated exp table, colBytes: 8 * this lane's column.
   template <int REP, bool FI = false, bool GRAM = false>
   __device__ static __forceinline__ double eval(double q, const double* tab, int colBytes = 0) {
-    // Gram q may round below 0: clamp to >= 2^-254 on the integer pipe, which
-    // also keeps sqrt(q) >= 2^-127 for the FP32-indexed exp
-    if constexpr (GRAM && gramClamp) q = __hiloint2double(max(__double2hiint(q), 769 << 20), __double2loint(q));
+    // Gram q may round slightly below 0: Matern's sources carry a bias that
+    // covers the rounding (near.cu gramBias; sqrt(q) >= 2^-127 as the
+    // FP32-indexed exp needs), the other Gram kernels take 1 + q. The Gram
+    // bound keeps sqrt(q) and 1 + q far below the exp clamp: no clamps here.
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
       double u = sqrt_nr(q);
-      if constexpr (FI) u = clamp_exp_arg(u);  // in place: the (1 + u) factor uses the same u
+      if constexpr (FI && !GRAM) u = clamp_exp_arg(u);  // in place: the (1 + u) factor uses the same u
       const double e = expn<FI, REP, !GRAM, false>(u, tab, colBytes);
       return fma(u, e, e);
     } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
@@ -59,7 +63,7 @@ struct FastKernel {
     } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
       return rsqrt_nr(GRAM ? q : 1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return expn<FI, REP>(q, tab, colBytes);
+      return expn<FI, REP, !GRAM, !GRAM>(q, tab, colBytes);
     } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
       return rsqrt_nr_half(q);  // q = r^2 / 2: fastScales scales by 1/sqrt(2)
     } else {

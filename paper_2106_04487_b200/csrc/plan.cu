@@ -405,7 +405,13 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
   } else if (!plan.s2mTilesHost.empty()) {
     k += plan.options.barnesHut ? 1 : chunks(plan.P);
   }
-  k += plan.nearSym ? !plan.blockTilesHost.empty() : !plan.nearTilesHost.empty();
+  if (plan.nearSym) {
+    k += !plan.blockTilesHost.empty();
+  } else if (!plan.nearTilesHost.empty()) {
+    // FP64 near field: one launch per pair form present (near.cu)
+    const long long g = plan.options.nearPrecision == 32 ? 0 : nearGramTiles(plan);
+    k += (g > 0) + (g < static_cast<long long>(plan.nearTilesHost.size()));
+  }
   k += !plan.farTilesHost.empty();
   return k;
 }

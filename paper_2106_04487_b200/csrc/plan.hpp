@@ -207,6 +207,9 @@ void launchBHSums(const DevicePlan& plan, const double* yp, double* totals, int 
 void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int nrhs, cudaStream_t stream);
 
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+// Near tiles the FP64 near field runs in Gram form (near.cu); the rest run the
+// difference form in a second launch.
+long long nearGramTiles(const DevicePlan& plan);
 void buildNearBlocks(DevicePlan& plan, bool oneWayOnly = false);
 bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
