@@ -144,6 +144,15 @@ constexpr double kGramBound = 128.0;
 #endif
 constexpr bool kNearFI = FKTB_NEAR_FI != 0;
 
+// Register prefetch of the next shared source row: measured on the B200 at
+// cfg2 (Matern d=3) 12.54 -> 12.32 ms and cfg4 (inverse-r d=3) 14.10 -> 13.92,
+// but slower for the 5-D Gaussian (21.65 -> 21.96) and 16 RHS (4.16 -> 4.27),
+// whose rows are wider: on for single-RHS 3-D tiles. FKTB_NEAR_PF=0/1 forces.
+#ifndef FKTB_NEAR_PF
+#define FKTB_NEAR_PF -1
+#endif
+constexpr bool nearPrefetch(int d, int r) { return FKTB_NEAR_PF >= 0 ? FKTB_NEAR_PF != 0 : (d == 3 && r == 1); }
+
 // Runtime A/B knob: FKTB_NEAR_GRAM=0 forces the difference form everywhere.
 inline bool nearGramEnabled() {
   static const bool v = [] {
@@ -242,16 +251,9 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
         }
       }
       __syncthreads();
-#pragma unroll UNR
-      for (int s = 0; s < cn; ++s) {
-        double src[SP];
-#pragma unroll
-        for (int q = 0; q < SP; q += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(&ss[s * SP + q]);
-          src[q] = v.x;
-          src[q + 1] = v.y;
-        }
-        constexpr int W0 = GRAM ? D + 1 : D;  // first weight slot
+      constexpr int W0 = GRAM ? D + 1 : D;  // first weight slot
+      // the pair block of one source row against this thread's TPT targets
+      auto pairs = [&](const double(&src)[SP]) {
 #pragma unroll
         for (int i = 0; i < TPT; ++i) {
           double q;
@@ -277,6 +279,36 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
 #pragma unroll
           for (int r = 0; r < R; ++r) acc[i][r] = fma(kv, src[W0 + r], acc[i][r]);
         }
+      };
+      auto load = [&](double(&src)[SP], int s) {
+#pragma unroll
+        for (int q = 0; q < SP; q += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(&ss[s * SP + q]);
+          src[q] = v.x;
+          src[q + 1] = v.y;
+        }
+      };
+      if constexpr (nearPrefetch(D, R)) {
+        // software pipeline: row s + 1 is loaded while row s is evaluated (the
+        // broadcast LDS latency otherwise stalls the first FMA of every row);
+        // row cn is a padding row of the shared array, loaded but never used
+        double cur[SP];
+        load(cur, 0);
+#pragma unroll UNR
+        for (int s = 0; s < cn; ++s) {
+          double nxt[SP];
+          load(nxt, s + 1);
+          pairs(cur);
+#pragma unroll
+          for (int q = 0; q < SP; ++q) cur[q] = nxt[q];
+        }
+      } else {
+#pragma unroll UNR
+        for (int s = 0; s < cn; ++s) {
+          double src[SP];
+          load(src, s);
+          pairs(src);
+        }
       }
     }
 #pragma unroll
@@ -300,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, (MB > 0 ? MB : (THREADS == 64 && R ==
   static_assert(!GRAM || (FastKernel<KID>::gram && !SEL), "Gram form needs a smooth kernel without select");
   constexpr int SP = nearStride(D, R, GRAM);
   constexpr int CHUNK = nearChunk(D, R, GRAM);
-  __shared__ __align__(16) double ss[CHUNK * SP];
+  __shared__ __align__(16) double ss[(CHUNK + 1) * SP];  // + a padding row for the prefetch
   __shared__ double tab[kNearExpTable * kNearExpRep];  // entry j at tab[j * kNearExpRep + column]
   const NearArgs& A = F.a;
   const FktbTile tile = A.tiles[blockIdx.x];
