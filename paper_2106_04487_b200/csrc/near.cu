@@ -167,7 +167,9 @@ inline bool nearGramEnabled() {
 // keep shared memory (and so occupancy) at the difference form's level; many
 // right-hand sides shrink the chunk to stay within 40 KB of static shared
 // memory next to the 8 KB exp table.
-constexpr int nearStride(int d, int r, bool gram) { return (d + (gram ? 1 : 0) + r + 1) / 2 * 2; }
+constexpr int nearStride(int d, int r, bool gram, bool factored = false) {
+  return (d + (gram && !factored ? 1 : 0) + r + 1) / 2 * 2;
+}
 constexpr int nearChunk(int d, int r, bool gram) {
   return gram ? (r > 2 ? 128 : 256) : (r <= 2 ? kFastChunk : (nearStride(d, r, false) * 256 * 8 <= 40960 ? 256 : 128));
 }
@@ -182,7 +184,8 @@ template <int KID, int D, bool SEL, int THREADS, int TPT, int UNR, int R, bool G
 __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& tile, double* ss, const double* tab,
                                           int colBytes) {
   using FK = FastKernel<KID>;
-  constexpr int SP = nearStride(D, R, GRAM);
+  constexpr bool FAC = GRAM && FK::gramFactored;
+  constexpr int SP = nearStride(D, R, GRAM, FAC);
   constexpr int CHUNK = nearChunk(D, R, GRAM);
   const NearArgs& A = F.a;
   const int leaf = tile.node;
@@ -191,7 +194,11 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
   double c[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) c[a] = GRAM ? F.center[static_cast<size_t>(leaf) * D + a] : 0.0;
-  const double wf = GRAM ? F.wf * FK::gramWeight : F.wf;  // weight prefactor of this form
+  const double wf = GRAM && !FAC ? F.wf * FK::gramWeight : F.wf;  // weight prefactor of this form
+  // factored Gaussian: q = Bt - 2 t.s >= 0 with Bt just above this tile's
+  // bound B >= |t|^2 + |s|^2 >= 2 t.s (the 1e-6 and 1e-30 margins cover the
+  // rounding and keep q >= 2^-127 for the FP32-indexed exp); q <= 2.1 B
+  const double Bt = FAC ? fma(1.000001 * kGramBound / F.gramLimit2, F.limit2[leaf], 1e-30) : 0.0;
   // Matern's Gram bias: q's rounding is <= (1.5 d + 0.5) eps B for this tile's
   // B = limit2 * kGramBound / gramLimit2 (|t|^2, |s|^2: d/2 eps B each; d FMAs
   // and one add: (d + 1)/2 eps B), so q + (1.5 d + 1) eps B + 1e-30 >= 1e-30
@@ -240,9 +247,15 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
             ns = fma(v, v, ns);
             ss[s * SP + a] = -2.0 * v;
           }
-          ss[s * SP + D] = ns + (FK::gramOffset + qbias);
+          if constexpr (FAC) {
+            const double ef = wf * exp(Bt - ns);  // e^(B - |s|^2) in [1, e^B]
 #pragma unroll
-          for (int r = 0; r < R; ++r) ss[s * SP + D + 1 + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * wf;
+            for (int r = 0; r < R; ++r) ss[s * SP + D + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * ef;
+          } else {
+            ss[s * SP + D] = ns + (FK::gramOffset + qbias);
+#pragma unroll
+            for (int r = 0; r < R; ++r) ss[s * SP + D + 1 + r] = A.yp[static_cast<size_t>(r0 + r) * n + cs + s] * wf;
+          }
         } else {
 #pragma unroll
           for (int a = 0; a < D; ++a) ss[s * SP + a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + cs + s], F.sc);
@@ -251,13 +264,17 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
         }
       }
       __syncthreads();
-      constexpr int W0 = GRAM ? D + 1 : D;  // first weight slot
+      constexpr int W0 = GRAM && !FAC ? D + 1 : D;  // first weight slot
       // the pair block of one source row against this thread's TPT targets
       auto pairs = [&](const double(&src)[SP]) {
 #pragma unroll
         for (int i = 0; i < TPT; ++i) {
           double q;
-          if constexpr (GRAM) {
+          if constexpr (FAC) {
+            q = fma(tx[i][0], src[0], Bt);
+#pragma unroll
+            for (int a = 1; a < D; ++a) q = fma(tx[i][a], src[a], q);
+          } else if constexpr (GRAM) {
             q = fma(tx[i][0], src[0], src[D]);
 #pragma unroll
             for (int a = 1; a < D; ++a) q = fma(tx[i][a], src[a], q);
@@ -313,9 +330,11 @@ __device__ __forceinline__ void near_tile(const FastArgs& F, const FktbTile& til
     }
 #pragma unroll
     for (int i = 0; i < TPT; ++i)
-      if (tpos[i] >= 0)
+      if (tpos[i] >= 0) {
+        const double tf = FAC ? exp(-tn[i]) : 1.0;  // factored Gaussian: e^-|t|^2
 #pragma unroll
-        for (int r = 0; r < R; ++r) atomicAdd(A.zp + static_cast<size_t>(r0 + r) * n + tpos[i], acc[i][r]);
+        for (int r = 0; r < R; ++r) atomicAdd(A.zp + static_cast<size_t>(r0 + r) * n + tpos[i], FAC ? acc[i][r] * tf : acc[i][r]);
+      }
   }
 }
 

@@ -33,6 +33,10 @@ struct FastKernel {
   static constexpr double gramOffset =
       KID == FKTB_KERNEL_CAUCHY || KID == FKTB_KERNEL_RATIONAL_QUADRATIC || KID == FKTB_KERNEL_GAUSSIAN ? 1.0 : 0.0;
   static constexpr double gramWeight = KID == FKTB_KERNEL_GAUSSIAN ? 2.718281828459045 : 1.0;
+  // Gaussian, factored Gram form (near.cu near_tile): e^-q = e^-|t|^2 *
+  // (e^(B - |s|^2) w) * e^-(B - 2 t.s), B the tile bound: d FMAs per pair and
+  // no add (the |t|^2 factor is applied once per target).
+  static constexpr bool gramFactored = KID == FKTB_KERNEL_GAUSSIAN;
   // Matern-3/2 takes sqrt(q): its Gram q gets an additive bias (near.cu).
   static constexpr bool gramBiased = KID == FKTB_KERNEL_MATERN32;
 
