@@ -58,7 +58,7 @@ def near_flops_per_pair(kernel: str, d: int) -> int:
 # roofline.frac can exceed 1 while the FP64 pipe is ~70% busy.
 EXEC_FP64_PER_PAIR = {
     ("matern32", 3, 1): (16, 27),   # Gram form: 11 DFMA, 3 DMUL, 2 DADD
-    ("gaussian", 5, 1): (13, 23),   # Gram form: 10 DFMA, 1 DMUL, 2 DADD
+    ("gaussian", 5, 1): (12, 22),   # factored Gram form: 10 DFMA, 1 DMUL, 1 DADD
     ("inverse-r", 3, 1): (10, 16),  # difference form + select: 6 DFMA, 1 DMUL, 3 DADD
     ("cauchy", 2, 16): (23, 45),    # Gram form, 16 RHS: 22 DFMA, 1 DADD
     ("cauchy", 3, 1): (9, 17),      # Gram form: 8 DFMA, 1 DADD
