@@ -9,6 +9,7 @@
 //               Z_k nrm^2 kappa^2; transposed copy for coalesced reads)
 // Compile-time (d, p) shapes only; other shapes keep the direct S2M (far.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_math.cuh"
 #include "plan.hpp"
@@ -104,6 +105,106 @@ __global__ void __launch_bounds__(kP2MMaxThreads) p2m_regs(const __grid_constant
   if (active) atomicAdd(A.mono + (static_cast<size_t>(rr) * A.nodes + leaf) * C + a, acc);
 }
 
+// Multi-RHS P2M: a warp per source stream (kP2MGroups warps split the tile's
+// sources), lane l owning monomials l, l + 32, ... for RB right-hand sides in
+// registers. Each (source, monomial) product x'^a is formed once (D broadcast
+// power loads) and feeds RB FMAs against the source's RB weights (RB/2
+// broadcast LDS.128), instead of RB x (D + 1 loads + D FP64 ops) with one
+// (rhs, monomial) per thread (p2m_regs). The groups' partial sums are reduced
+// in shared memory, one atomic per (rhs, monomial) per tile.
+constexpr int kP2MGroups = 8;
+template <int D, int P, int RB>
+__global__ void __launch_bounds__(32 * kP2MGroups) p2m_multi(const __grid_constant__ MomArgs A) {
+  constexpr int C = mono_count(D, P);
+  constexpr int PW = P + 1;
+  constexpr int AM = (C + 31) / 32;  // monomials per lane
+  constexpr int CH = 64;             // sources staged per pass
+  __shared__ double spw[CH * D * PW];                // [src][axis][power]
+  __shared__ __align__(16) double sw[CH * RB];       // [src][rhs]
+  __shared__ double sred[AM * RB * 32];              // the groups' partial sums, reduced in turn
+  const FktbTile tile = A.tiles[blockIdx.x];
+  const int leaf = tile.node;
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  int off[AM][D];
+  bool own[AM];
+#pragma unroll
+  for (int m = 0; m < AM; ++m) {
+    const int a = lane + 32 * m;
+    own[m] = a < C;
+#pragma unroll
+    for (int q = 0; q < D; ++q) off[m][q] = q * PW + (own[m] ? A.exps[a * D + q] : 0);
+  }
+  double c[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) c[q] = A.center[static_cast<size_t>(leaf) * D + q];
+  for (int r0 = 0; r0 < A.nrhs; r0 += RB) {
+    double acc[AM][RB];
+#pragma unroll
+    for (int m = 0; m < AM; ++m)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[m][r] = 0.0;
+    for (int s0 = 0; s0 < tile.count; s0 += CH) {
+      const int cn = min(CH, tile.count - s0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cn * D; t += blockDim.x) {
+        const int s = t / D, q = t % D;
+        const int pos = static_cast<int>(tile.start) + s0 + s;
+        const double x = A.pc[static_cast<size_t>(q) * A.n + pos] - c[q];
+        double* row = spw + (s * D + q) * PW;
+        double v = 1.0;
+        row[0] = 1.0;
+#pragma unroll
+        for (int e = 1; e <= P; ++e) {
+          v *= x;
+          row[e] = v;
+        }
+      }
+      for (int t = threadIdx.x; t < cn * RB; t += blockDim.x) {
+        const int s = t / RB, r = t % RB;
+        sw[t] = A.yp[static_cast<size_t>(r0 + r) * A.n + tile.start + s0 + s];
+      }
+      __syncthreads();
+      for (int s = grp; s < cn; s += kP2MGroups) {
+        const double* pw = spw + s * D * PW;
+        double w[RB];
+#pragma unroll
+        for (int r = 0; r < RB; r += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(sw + s * RB + r);
+          w[r] = v.x;
+          w[r + 1] = v.y;
+        }
+#pragma unroll
+        for (int m = 0; m < AM; ++m) {
+          double mono = pw[off[m][0]];
+#pragma unroll
+          for (int q = 1; q < D; ++q) mono *= pw[off[m][q]];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) acc[m][r] = fma(mono, w[r], acc[m][r]);
+        }
+      }
+    }
+    // reduce the groups' partial sums in turn (fixed order), then one atomic
+    // per (rhs, monomial)
+    for (int g2 = 0; g2 < kP2MGroups; ++g2) {
+      __syncthreads();
+      if (grp == g2)
+#pragma unroll
+        for (int m = 0; m < AM; ++m)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            double& dst = sred[(m * RB + r) * 32 + lane];
+            dst = g2 == 0 ? acc[m][r] : dst + acc[m][r];
+          }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < AM * RB * 32; i += blockDim.x) {
+      const int l = i & 31, mr = i >> 5, m = mr / RB, r = mr % RB;
+      const int a = l + 32 * m;
+      if (a < C) atomicAdd(A.mono + (static_cast<size_t>(r0 + r) * A.nodes + leaf) * C + a, sred[i]);
+    }
+  }
+}
+
 // Shift tables (CSR over the output monomial) staged in shared memory once
 // per CTA; each CTA then walks parents blockIdx.x, blockIdx.x + gridDim.x, ...
 template <int D>
@@ -184,6 +285,14 @@ __global__ void __launch_bounds__(128) to_coef_gemm(const double* mono, const do
   }
 }
 
+// Multi-RHS P2M block size: RB right-hand sides per pass with AM x RB <= 48
+// register accumulators per lane (0: not applicable, keep p2m_regs).
+template <int D, int P>
+constexpr int p2mMultiBlock() {
+  constexpr int AM = (mono_count(D, P) + 31) / 32;
+  return AM * 16 <= 48 ? 16 : (AM * 8 <= 48 ? 8 : 0);
+}
+
 template <int D, int P>
 void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   constexpr int C = mono_count(D, P);
@@ -192,6 +301,30 @@ void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   p2m_regs<D, P><<<tiles, threads, smem, st>>>(A);
   FKTB_CUDA(cudaGetLastError());
 }
+
+// Developer A/B knob: FKTB_P2M_MULTI=0 keeps multi-RHS P2M on p2m_regs.
+inline bool p2mMultiEnabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("FKTB_P2M_MULTI");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+template <int D, int P>
+bool launchP2MMulti(const MomArgs& A, int tiles, cudaStream_t st) {
+  constexpr int RB = p2mMultiBlock<D, P>();
+  if constexpr (RB == 0) {
+    return false;
+  } else {
+    if (A.nrhs % RB != 0) return false;
+    p2m_multi<D, P, RB><<<tiles, 32 * kP2MGroups, 0, st>>>(A);
+    FKTB_CUDA(cudaGetLastError());
+    return true;
+  }
+}
+
+
 
 template <int D>
 void launchM2M(const MomArgs& A, int parents, int entries, cudaStream_t st) {
@@ -205,6 +338,23 @@ void launchM2M(const MomArgs& A, int parents, int entries, cudaStream_t st) {
 }
 
 }  // namespace
+
+// P2M launches of one multiply (kernelLaunches): one p2m_multi launch when the
+// RHS-blocked path applies, else one p2m_regs launch per RHS chunk.
+int p2mLaunches(int d, int p, int count, int nrhs) {
+  int rb = 0;
+  switch (d * 100 + p) {
+    case 206: rb = p2mMultiBlock<2, 6>(); break;
+    case 304: rb = p2mMultiBlock<3, 4>(); break;
+    case 306: rb = p2mMultiBlock<3, 6>(); break;
+    case 308: rb = p2mMultiBlock<3, 8>(); break;
+    case 504: rb = p2mMultiBlock<5, 4>(); break;
+    default: break;
+  }
+  if (rb > 0 && nrhs >= 8 && nrhs % rb == 0 && p2mMultiEnabled()) return 1;
+  const int chunk = std::max(1, kP2MMaxThreads / count);
+  return (nrhs + chunk - 1) / chunk;
+}
 
 bool momentsSupported(int d, int p) {
   switch (d * 100 + p) {
@@ -244,7 +394,24 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   // right-hand sides to fit.
   const int chunk = std::max(1, kP2MMaxThreads / C);
   const int tiles = static_cast<int>(plan.p2mTilesHost.size());
-  for (int r0 = 0; r0 < nrhs && tiles > 0; r0 += chunk) {
+  // many right-hand sides: RHS-blocked p2m_multi (monomial formed once per
+  // source and reused for the block)
+  auto multi = [&]() -> bool {
+    if (tiles == 0 || nrhs < 8 || !p2mMultiEnabled()) return false;
+    MomArgs B = A;
+    B.nrhs = nrhs;
+    B.yp = yp;
+    switch (plan.d * 100 + plan.options.p) {
+      case 206: return launchP2MMulti<2, 6>(B, tiles, st);
+      case 304: return launchP2MMulti<3, 4>(B, tiles, st);
+      case 306: return launchP2MMulti<3, 6>(B, tiles, st);
+      case 308: return launchP2MMulti<3, 8>(B, tiles, st);
+      case 504: return launchP2MMulti<5, 4>(B, tiles, st);
+      default: return false;
+    }
+  };
+  const bool didMulti = multi();
+  for (int r0 = 0; r0 < nrhs && tiles > 0 && !didMulti; r0 += chunk) {
     MomArgs B = A;
     B.nrhs = std::min(chunk, nrhs - r0);
     B.yp = yp + static_cast<size_t>(r0) * t.n;

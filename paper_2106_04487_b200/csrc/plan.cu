@@ -396,10 +396,7 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
   };
   long long k = 2;  // gather_y, scatter_z
   if (plan.useMoments) {
-    if (!plan.p2mTilesHost.empty()) {  // p2m: <= 8 x 128 register accumulators per launch
-      const int chunk = std::max(1, 8 * 128 / plan.monoCount);
-      k += (nrhs + chunk - 1) / chunk;
-    }
+    if (!plan.p2mTilesHost.empty()) k += p2mLaunches(plan.d, plan.options.p, plan.monoCount, nrhs);
     for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
     k += !plan.farNodesHost.empty();  // to_coef (one GEMM over all nodes)
   } else if (!plan.s2mTilesHost.empty()) {

@@ -217,6 +217,8 @@ bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 void launchS2M(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
 bool momentsSupported(int d, int p);
+// P2M launches of one multiply with nrhs right-hand sides (moments.cu).
+int p2mLaunches(int d, int p, int count, int nrhs);
 void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
 // Monomial-moment S2M when the plan has it, else the direct S2M.
 void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int nrhs, cudaStream_t stream);
