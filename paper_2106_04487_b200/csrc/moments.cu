@@ -167,11 +167,15 @@ __global__ void __launch_bounds__(32 * kP2MGroups) p2m_multi(const __grid_consta
       for (int s = grp; s < cn; s += kP2MGroups) {
         const double* pw = spw + s * D * PW;
         double w[RB];
+        if constexpr (RB == 1) {
+          w[0] = sw[s];
+        } else {
 #pragma unroll
-        for (int r = 0; r < RB; r += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(sw + s * RB + r);
-          w[r] = v.x;
-          w[r + 1] = v.y;
+          for (int r = 0; r < RB; r += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(sw + s * RB + r);
+            w[r] = v.x;
+            w[r + 1] = v.y;
+          }
         }
 #pragma unroll
         for (int m = 0; m < AM; ++m) {
@@ -302,6 +306,15 @@ void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   FKTB_CUDA(cudaGetLastError());
 }
 
+// Developer A/B knob: FKTB_P2M_SINGLE=1 runs single-RHS P2M on p2m_multi too.
+inline bool p2mSingleMulti() {
+  static const bool v = [] {
+    const char* e = std::getenv("FKTB_P2M_SINGLE");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // Developer A/B knob: FKTB_P2M_MULTI=0 keeps multi-RHS P2M on p2m_regs.
 inline bool p2mMultiEnabled() {
   static const bool v = [] {
@@ -317,6 +330,11 @@ bool launchP2MMulti(const MomArgs& A, int tiles, cudaStream_t st) {
   if constexpr (RB == 0) {
     return false;
   } else {
+    if (A.nrhs == 1 && p2mSingleMulti()) {  // single RHS: 8 source streams x AM monomials per lane
+      p2m_multi<D, P, 1><<<tiles, 32 * kP2MGroups, 0, st>>>(A);
+      FKTB_CUDA(cudaGetLastError());
+      return true;
+    }
     if (A.nrhs % RB != 0) return false;
     p2m_multi<D, P, RB><<<tiles, 32 * kP2MGroups, 0, st>>>(A);
     FKTB_CUDA(cudaGetLastError());
@@ -397,7 +415,7 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   // many right-hand sides: RHS-blocked p2m_multi (monomial formed once per
   // source and reused for the block)
   auto multi = [&]() -> bool {
-    if (tiles == 0 || nrhs < 8 || !p2mMultiEnabled()) return false;
+    if (tiles == 0 || (nrhs < 8 && !(nrhs == 1 && p2mSingleMulti())) || !p2mMultiEnabled()) return false;
     MomArgs B = A;
     B.nrhs = nrhs;
     B.yp = yp;
