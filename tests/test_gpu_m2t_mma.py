@@ -31,3 +31,26 @@ def test_mma_m2t_columns(fkt, ref, name, prm, d, p, nrhs, comp):
         col = np.ascontiguousarray(W[:, c])
         assert fkt.relativeError(Z[:, c], rp.multiply(col)) <= 1e-10, (c,)
         assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 1e-13, (c,)
+
+
+@pytest.mark.parametrize("name,prm,d,p,nrhs,comp", [
+    ("matern32", {"sigma": 1.0, "rho": 0.3}, 3, 6, 16, None),  # P2M RB = 16 (3 monomials / lane); M2T DFMA (P > 64)
+    ("inverse-r", {}, 3, 8, 8, "on"),                           # P2M RB = 8 (6 monomials / lane)
+    ("gaussian", {}, 5, 4, 8, "on"),                            # P2M RB = 8 (4 monomials / lane)
+])
+def test_rhs_blocked_p2m_columns(fkt, ref, name, prm, d, p, nrhs, comp):
+    # RHS-blocked P2M (csrc/moments.cu p2m_multi) at the remaining moment
+    # shapes: every column against the reference and the single-RHS path
+    rng = np.random.default_rng(22)
+    n = 10000
+    x = rng.random((n, d))
+    W = rng.standard_normal((n, nrhs))
+    mode = {None: fkt.CompressionMode.Auto, "on": fkt.CompressionMode.On}[comp]
+    pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(name, prm),
+                  fkt.FktOptions(p=p, theta=0.6, leafCapacity=256, compression=mode))
+    Z = pl.multiply(W)
+    rp = ref.RefPlan(x, name, prm, p=p, theta=0.6, leaf=256, compression=int(mode))
+    for c in (0, nrhs // 2, nrhs - 1):
+        col = np.ascontiguousarray(W[:, c])
+        assert fkt.relativeError(Z[:, c], rp.multiply(col)) <= 1e-10, (c,)
+        assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 1e-13, (c,)
