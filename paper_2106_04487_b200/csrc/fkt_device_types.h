@@ -102,7 +102,7 @@ typedef struct FktbBlockTile {
   int rowCount;
   int colCount;
   int sym;
-  int pad_;
+  int leaf;  // leaf whose centre and bound the Gram form of this block uses
 } FktbBlockTile;
 
 #endif

@@ -23,6 +23,7 @@
 // partial to shared memory and the column sums go to z with one atomic per
 // column per tile.
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "fastmath.cuh"
@@ -166,6 +167,148 @@ bool launchSymK(const SymArgs& A, int d, bool sel, int tiles, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric blocks in the Gram form (near.cu near_tile): one
+// warp per tile, lane owning rows lane + 32 i (i < G, G = ceil(rows / 32)
+// chosen per tile by a switch so every instantiation keeps G independent
+// chains); columns staged in shared memory 128 at a time as (-2 s, |s|^2 +
+// offset + bias, weight). In symmetric tiles each lane also accumulates
+// K(t_i, s) y_t over its rows; a 5-step butterfly gives the column sum, and
+// the chunk's column sums go to z with one atomic per column.
+struct SymGArgs {
+  int n;
+  const double* pc;
+  const uint32_t* pool;
+  const FktbBlockTile* tiles;
+  const double* yp;
+  double* zp;
+  const double* expTable;
+  double sc, wf;
+  const double* center;
+  const double* limit2;
+  double gramLimit2;  // tile bound B = limit2[leaf] * kGramBoundSym / gramLimit2
+};
+
+constexpr double kGramBoundSym = 128.0;  // as near.cu kGramBound
+constexpr int kSymGChunk = 128;
+
+template <int KID, int D, bool SYM, int G>
+__device__ __forceinline__ void gram_block(const SymGArgs& A, const FktbBlockTile& tile, double* ss, double* colbuf,
+                                           int* colpos, const double* tab) {
+  using FK = FastKernel<KID>;
+  constexpr int SP = (D + 2 + 1) / 2 * 2;
+  const int n = A.n;
+  const int lane = threadIdx.x & 31;
+  const int leaf = tile.leaf;
+  double c[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) c[a] = A.center[static_cast<size_t>(leaf) * D + a];
+  const double wfG = A.wf * FK::gramWeight;
+  const double qbias = FK::gramBiased
+                           ? fma((1.5 * D + 1.0) * 2.220446049250313e-16 * kGramBoundSym / A.gramLimit2, A.limit2[leaf], 1e-30)
+                           : 0.0;
+  int tpos[G];
+  double tx[G][D], tn[G], ty[G], acc[G];
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const int idx = i * 32 + lane;
+    tpos[i] = idx < tile.rowCount ? static_cast<int>(A.pool[tile.rowOff + idx]) : -1;
+    const int p = tpos[i] >= 0 ? tpos[i] : static_cast<int>(A.pool[tile.rowOff]);  // dead lanes: a copy of row 0
+    tn[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      tx[i][a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + p] - c[a], A.sc);
+      tn[i] = fma(tx[i][a], tx[i][a], tn[i]);
+    }
+    ty[i] = SYM && tpos[i] >= 0 ? A.yp[p] * wfG : 0.0;
+    acc[i] = 0.0;
+  }
+  for (int cs = 0; cs < tile.colCount; cs += kSymGChunk) {
+    const int cn = min(kSymGChunk, tile.colCount - cs);
+    __syncwarp();
+    for (int s = lane; s < cn; s += 32) {
+      const int pos = static_cast<int>(A.pool[tile.colOff + cs + s]);
+      double ns = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double v = __dmul_rn(A.pc[static_cast<size_t>(a) * n + pos] - c[a], A.sc);
+        ns = fma(v, v, ns);
+        ss[s * SP + a] = -2.0 * v;
+      }
+      ss[s * SP + D] = ns + (FK::gramOffset + qbias);
+      ss[s * SP + D + 1] = A.yp[pos] * wfG;
+      if constexpr (SYM) colpos[s] = pos;
+    }
+    __syncwarp();
+#pragma unroll 2
+    for (int s = 0; s < cn; ++s) {
+      double src[SP];
+#pragma unroll
+      for (int q = 0; q < SP; q += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&ss[s * SP + q]);
+        src[q] = v.x;
+        src[q + 1] = v.y;
+      }
+      double cp = 0.0;
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        double q = fma(tx[i][0], src[0], src[D]);
+#pragma unroll
+        for (int a = 1; a < D; ++a) q = fma(tx[i][a], src[a], q);
+        q += tn[i];
+        const double kv = FK::template eval<kNearExpRep, true, true>(q, tab, 0);
+        acc[i] = fma(kv, src[D + 1], acc[i]);
+        if constexpr (SYM) cp = fma(kv, ty[i], cp);
+      }
+      if constexpr (SYM) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cp += __shfl_xor_sync(0xffffffffu, cp, o);
+        if (lane == (s & 31)) colbuf[s] = cp;
+      }
+    }
+    if constexpr (SYM) {
+      __syncwarp();
+      for (int s = lane; s < cn; s += 32) atomicAdd(A.zp + colpos[s], colbuf[s]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < G; ++i)
+    if (tpos[i] >= 0) atomicAdd(A.zp + tpos[i], acc[i]);
+}
+
+template <int KID, int D, bool SYM>
+__device__ __forceinline__ void gram_block_g(const SymGArgs& A, const FktbBlockTile& tile, double* ss, double* colbuf,
+                                             int* colpos, const double* tab) {
+  switch ((tile.rowCount + 31) >> 5) {  // warp-uniform
+    case 1: return gram_block<KID, D, SYM, 1>(A, tile, ss, colbuf, colpos, tab);
+    case 2: return gram_block<KID, D, SYM, 2>(A, tile, ss, colbuf, colpos, tab);
+    case 3: return gram_block<KID, D, SYM, 3>(A, tile, ss, colbuf, colpos, tab);
+    case 4: return gram_block<KID, D, SYM, 4>(A, tile, ss, colbuf, colpos, tab);
+    case 5: return gram_block<KID, D, SYM, 5>(A, tile, ss, colbuf, colpos, tab);
+    case 6: return gram_block<KID, D, SYM, 6>(A, tile, ss, colbuf, colpos, tab);
+    case 7: return gram_block<KID, D, SYM, 7>(A, tile, ss, colbuf, colpos, tab);
+    default: return gram_block<KID, D, SYM, 8>(A, tile, ss, colbuf, colpos, tab);
+  }
+}
+
+template <int KID, int D>
+__global__ void __launch_bounds__(32) near_sym_gram(const __grid_constant__ SymGArgs A) {
+  static_assert(kSymRows == 256, "block tiles of 256 rows = 32 lanes x 8");
+  constexpr int SP = (D + 2 + 1) / 2 * 2;
+  __shared__ __align__(16) double ss[kSymGChunk * SP];
+  __shared__ double colbuf[kSymGChunk];
+  __shared__ int colpos[kSymGChunk];
+  __shared__ double tab[kNearExpTable * kNearExpRep];
+  if constexpr (FastKernel<KID>::needsTable)
+    for (int i = threadIdx.x; i < kNearExpTable * kNearExpRep; i += 32) tab[i] = A.expTable[i / kNearExpRep];
+  __syncwarp();
+  const FktbBlockTile tile = A.tiles[blockIdx.x];
+  if (tile.sym)
+    gram_block_g<KID, D, true>(A, tile, ss, colbuf, colpos, tab);
+  else
+    gram_block_g<KID, D, false>(A, tile, ss, colbuf, colpos, tab);
+}
+
 bool symSupported(int kid, int d) {
   const bool k = kid == FKTB_KERNEL_MATERN32 || kid == FKTB_KERNEL_MATERN12 || kid == FKTB_KERNEL_EXPONENTIAL ||
                  kid == FKTB_KERNEL_CAUCHY || kid == FKTB_KERNEL_RATIONAL_QUADRATIC || kid == FKTB_KERNEL_GAUSSIAN ||
@@ -211,10 +354,10 @@ void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
   std::vector<uint32_t> comp;  // complements, appended after identity
   std::vector<FktbBlockTile> tiles;
   long long symPairs = 0, oneWay = 0;
-  auto addBlock = [&](long long rowOff, int rowCount, long long colOff, int colCount, int sym) {
+  auto addBlock = [&](long long rowOff, int rowCount, long long colOff, int colCount, int sym, int leaf) {
     if (rowCount <= 0 || colCount <= 0) return;
     for (int r = 0; r < rowCount; r += kSymRows)
-      tiles.push_back(FktbBlockTile{rowOff + r, colOff, std::min(kSymRows, rowCount - r), colCount, sym, 0});
+      tiles.push_back(FktbBlockTile{rowOff + r, colOff, std::min(kSymRows, rowCount - r), colCount, sym, leaf});
     (sym ? symPairs : oneWay) += static_cast<long long>(rowCount) * colCount;
   };
   auto complement = [&](int leaf, const Seg& sub) {
@@ -236,7 +379,7 @@ void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
     const int aCount = static_cast<int>(t.end[static_cast<size_t>(A)] - t.begin[static_cast<size_t>(A)]);
     if (oneWayOnly) {  // A/B: the same kernel on the plain leaf decomposition
       addBlock(t.nearOff[static_cast<size_t>(A)], static_cast<int>(t.nearOff[static_cast<size_t>(A) + 1] - t.nearOff[static_cast<size_t>(A)]),
-               identityBase + aBegin, aCount, 0);
+               identityBase + aBegin, aCount, 0, A);
       continue;
     }
     // rows that need all of A's sources: A's own and non-mutual targets, merged
@@ -245,7 +388,7 @@ void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
       if (B == A || seg.find(key(B, A)) == seg.end())
         comp.insert(comp.end(), nearPos.begin() + sAB.off, nearPos.begin() + sAB.off + sAB.len);
     addBlock(fullBase, static_cast<int>(identityBase + n + static_cast<long long>(comp.size()) - fullBase),
-             identityBase + aBegin, aCount, 0);
+             identityBase + aBegin, aCount, 0, A);
     for (const auto& [B, sAB] : segsOf[static_cast<size_t>(A)]) {
       if (B == A) continue;
       auto it = seg.find(key(B, A));
@@ -254,11 +397,13 @@ void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
       const Seg& sBA = it->second;  // rows in A that need B's sources
       const long long bBegin = t.begin[static_cast<size_t>(B)];
       (void)bBegin;
-      addBlock(sAB.off, sAB.len, sBA.off, sBA.len, 1);  // rows T_AB (in B) x cols T_BA (in A)
+      // rows T_AB (in B, near A) x cols T_BA (in A): centred on A, whose
+      // bound covers both (rows within radius_A / theta, cols within radius_A)
+      addBlock(sAB.off, sAB.len, sBA.off, sBA.len, 1, A);
       const auto cA = complement(A, sBA);              // A \ T_BA
-      addBlock(sAB.off, sAB.len, cA.first, cA.second, 0);
+      addBlock(sAB.off, sAB.len, cA.first, cA.second, 0, A);
       const auto cB = complement(B, sAB);              // B \ T_AB
-      addBlock(sBA.off, sBA.len, cB.first, cB.second, 0);
+      addBlock(sBA.off, sBA.len, cB.first, cB.second, 0, B);
     }
   }
   // Longest tiles first: the heavy symmetric blocks start early.
@@ -289,6 +434,29 @@ void buildNearBlocks(DevicePlan& plan, bool oneWayOnly) {
   plan.nearSym = true;
 }
 
+// The Gram-form symmetric kernel serves the smooth kernels without an r == 0
+// select when every block's leaf passes the Gram bound (else the difference
+// form below); FKTB_NEAR_SYM_DIFF=1 forces the difference form (A/B).
+template <int KID>
+bool launchSymGramK(const DevicePlan& plan, const double* yp, double* zp, double sc, double wf, int tiles,
+                    cudaStream_t st) {
+  const DeviceTree& t = *plan.tree;
+  SymGArgs A{plan.n, t.pc.get(), plan.dNearPool.get(), plan.dBlockTiles.get(), yp, zp, expTableDevice(kNearExpBits),
+             sc, wf, t.dCenter.get(), t.dLimit2.get(), kGramBoundSym / (sc * sc * (1.0 + t.theta * t.theta))};
+  for (const FktbBlockTile& tl : plan.blockTilesHost) {
+    volatile double limit = t.radius[static_cast<size_t>(tl.leaf)] / t.theta;
+    if (!(limit * limit <= A.gramLimit2)) return false;
+  }
+  switch (plan.d) {
+    case 2: near_sym_gram<KID, 2><<<tiles, 32, 0, st>>>(A); break;
+    case 3: near_sym_gram<KID, 3><<<tiles, 32, 0, st>>>(A); break;
+    case 5: near_sym_gram<KID, 5><<<tiles, 32, 0, st>>>(A); break;
+    default: return false;
+  }
+  FKTB_CUDA(cudaGetLastError());
+  return true;
+}
+
 bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
   if (!plan.nearSym || nrhs != 1 || plan.options.nearPrecision != 64) return false;
   const int tiles = static_cast<int>(plan.blockTilesHost.size());
@@ -296,6 +464,29 @@ bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrh
   FktbKernelDesc kd;
   fillKernelDesc(plan.kernel, kd);
   if (plan.options.hasDiagonal) kd.diag = plan.options.diagonal;
+  {
+    double sc, wf;
+    fastScales(kd, sc, wf);
+    const char* e = std::getenv("FKTB_NEAR_SYM_DIFF");
+    const bool forceDiff = e && e[0] == '1';
+    if (!forceDiff && kd.diag == wf) {
+      switch (kd.id) {
+        case FKTB_KERNEL_MATERN32:
+          if (launchSymGramK<FKTB_KERNEL_MATERN32>(plan, yp, zp, sc, wf, tiles, st)) return true;
+          break;
+        case FKTB_KERNEL_CAUCHY:
+          if (launchSymGramK<FKTB_KERNEL_CAUCHY>(plan, yp, zp, sc, wf, tiles, st)) return true;
+          break;
+        case FKTB_KERNEL_RATIONAL_QUADRATIC:
+          if (launchSymGramK<FKTB_KERNEL_RATIONAL_QUADRATIC>(plan, yp, zp, sc, wf, tiles, st)) return true;
+          break;
+        case FKTB_KERNEL_GAUSSIAN:
+          if (launchSymGramK<FKTB_KERNEL_GAUSSIAN>(plan, yp, zp, sc, wf, tiles, st)) return true;
+          break;
+        default: break;
+      }
+    }
+  }
   SymArgs A{plan.n, plan.tree->pc.get(), plan.dNearPool.get(), plan.dBlockTiles.get(), yp, zp, expTableDevice(kNearExpBits),
             1.0, 1.0, 0.0};
   fastScales(kd, A.sc, A.wf);
