@@ -260,6 +260,51 @@ __global__ void m2m_kernel(const __grid_constant__ MomArgs A, int parents, int e
   }
 }
 
+// The narrow top of the tree in one launch: CTA per (node b, frontier node f)
+// adds Shift(c_f - c_b) mu_f into mu_b (atomics; mu_b starts at zero from the
+// S2M memset). The monomial shift is the M2M's with an arbitrary delta, so a
+// composite shift over several levels is exact up to rounding:
+// mu_b[a] = sum_f sum_{e in CSR(a)} coef_e delta_f^g_e mu_f[b_e].
+template <int D>
+__global__ void m2m_pairs(const __grid_constant__ MomArgs A, const int* pairs, int entries) {
+  extern __shared__ double sm[];  // coef[E] | dpow[C] | mu[nrhs][C] | off[C+1] b[E] g[E] (ints)
+  const int C = A.count;
+  double* scoef = sm;
+  double* dpow = scoef + entries;
+  double* mu = dpow + C;
+  int* soff = reinterpret_cast<int*>(mu + A.nrhs * C);
+  int* sb = soff + C + 1;
+  int* sg = sb + entries;
+  const int b = pairs[2 * blockIdx.x], f = pairs[2 * blockIdx.x + 1];
+  for (int i = threadIdx.x; i < entries; i += blockDim.x) {
+    scoef[i] = A.coef[i];
+    sb[i] = A.b[i];
+    sg[i] = A.g[i];
+  }
+  for (int i = threadIdx.x; i <= C; i += blockDim.x) soff[i] = A.off[i];
+  for (int a = threadIdx.x; a < C; a += blockDim.x) {
+    double v = 1.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      const double delta = A.center[static_cast<size_t>(f) * D + q] - A.center[static_cast<size_t>(b) * D + q];
+      for (int e = 0; e < A.exps[a * D + q]; ++e) v *= delta;
+    }
+    dpow[a] = v;
+  }
+  for (int i = threadIdx.x; i < A.nrhs * C; i += blockDim.x) {
+    const int r = i / C, a = i % C;
+    mu[i] = A.mono[(static_cast<size_t>(r) * A.nodes + f) * C + a];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < A.nrhs * C; i += blockDim.x) {
+    const int r = i / C, a = i % C;
+    const double* m = mu + static_cast<size_t>(r) * C;
+    double acc = 0.0;
+    for (int e = soff[a]; e < soff[a + 1]; ++e) acc = fma(scoef[e] * dpow[sg[e]], m[sb[e]], acc);
+    atomicAdd(A.mono + (static_cast<size_t>(r) * A.nodes + b) * C + a, acc);
+  }
+}
+
 // Node moments in the FKT basis for every (rhs, node) row: out[R][P] =
 // mono[R][C] * TT[C][P] -- a small GEMM, 32 rows per CTA staged in shared
 // memory, TT columns read coalesced (same for every CTA: L1/L2 resident).
@@ -343,6 +388,14 @@ bool launchP2MMulti(const MomArgs& A, int tiles, cudaStream_t st) {
 }
 
 
+
+template <int D>
+void launchM2MPairs(const MomArgs& A, const int* pairs, int npairs, int entries, size_t smem, cudaStream_t st) {
+  if (smem > 48 * 1024)
+    FKTB_CUDA(cudaFuncSetAttribute(m2m_pairs<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  m2m_pairs<D><<<npairs, 256, smem, st>>>(A, pairs, entries);
+  FKTB_CUDA(cudaGetLastError());
+}
 
 template <int D>
 void launchM2M(const MomArgs& A, int parents, int entries, cudaStream_t st) {
@@ -446,7 +499,7 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   // K4b: bottom-up shifts, deepest internal level first.
   A.nrhs = nrhs;
   A.yp = yp;
-  for (int lv = static_cast<int>(plan.levelOff.size()) - 2; lv >= 0; --lv) {
+  for (int lv = static_cast<int>(plan.levelOff.size()) - 2; lv >= plan.m2mTop; --lv) {
     const int a0 = plan.levelOff[static_cast<size_t>(lv)], a1 = plan.levelOff[static_cast<size_t>(lv) + 1];
     if (a1 == a0) continue;
     MomArgs B = A;
@@ -455,6 +508,17 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
       case 2: launchM2M<2>(B, a1 - a0, plan.shiftEntries, st); break;
       case 3: launchM2M<3>(B, a1 - a0, plan.shiftEntries, st); break;
       case 5: launchM2M<5>(B, a1 - a0, plan.shiftEntries, st); break;
+      default: throw std::logic_error("monomial S2M: unsupported dimension");
+    }
+  }
+  if (plan.topPairs > 0) {  // the narrow top levels from their frontier, one launch
+    MomArgs B = A;
+    const size_t smem = static_cast<size_t>(plan.shiftEntries + C * (1 + nrhs)) * sizeof(double) +
+                        static_cast<size_t>(C + 1 + 2 * plan.shiftEntries) * sizeof(int);
+    switch (plan.d) {
+      case 2: launchM2MPairs<2>(B, plan.dTopPairs.get(), plan.topPairs, plan.shiftEntries, smem, st); break;
+      case 3: launchM2MPairs<3>(B, plan.dTopPairs.get(), plan.topPairs, plan.shiftEntries, smem, st); break;
+      case 5: launchM2MPairs<5>(B, plan.dTopPairs.get(), plan.topPairs, plan.shiftEntries, smem, st); break;
       default: throw std::logic_error("monomial S2M: unsupported dimension");
     }
   }

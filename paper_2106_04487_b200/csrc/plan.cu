@@ -258,6 +258,28 @@ void buildMomentPlan(DevicePlan& plan) {
   }
   uploadVec(plan.dLevelNodes, levelNodes, st);
   uploadVec(plan.dFarNodes, plan.farNodesHost, st);
+  // top levels by composite shifts from the depth-m2mTop frontier (moments.cu
+  // m2m_pairs): one launch instead of one latency-bound launch per level
+  constexpr int kM2MTopDepth = 6;
+  plan.m2mTop = std::min(kM2MTopDepth, maxDepth);
+  std::vector<int> topPairs;
+  for (int b = 0; b < t.nodes; ++b) {
+    if (t.left[static_cast<size_t>(b)] < 0 || depth[static_cast<size_t>(b)] >= plan.m2mTop) continue;
+    std::vector<int> stack{t.left[static_cast<size_t>(b)], t.right[static_cast<size_t>(b)]};
+    while (!stack.empty()) {
+      const int f = stack.back();
+      stack.pop_back();
+      if (depth[static_cast<size_t>(f)] >= plan.m2mTop || t.left[static_cast<size_t>(f)] < 0) {
+        topPairs.push_back(b);
+        topPairs.push_back(f);
+      } else {
+        stack.push_back(t.left[static_cast<size_t>(f)]);
+        stack.push_back(t.right[static_cast<size_t>(f)]);
+      }
+    }
+  }
+  plan.topPairs = static_cast<int>(topPairs.size() / 2);
+  uploadVec(plan.dTopPairs, topPairs, st);
   plan.useMoments = true;
   buildP2MTiles(plan);
 }
@@ -397,7 +419,9 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
   long long k = 2;  // gather_y, scatter_z
   if (plan.useMoments) {
     if (!plan.p2mTilesHost.empty()) k += p2mLaunches(plan.d, plan.options.p, plan.monoCount, nrhs);
-    for (size_t l = 0; l + 1 < plan.levelOff.size(); ++l) k += plan.levelOff[l + 1] > plan.levelOff[l];  // m2m
+    for (size_t l = static_cast<size_t>(plan.m2mTop); l + 1 < plan.levelOff.size(); ++l)  // m2m, wide levels
+      k += plan.levelOff[l + 1] > plan.levelOff[l];
+    k += plan.topPairs > 0;  // m2m_pairs, the narrow top
     k += !plan.farNodesHost.empty();  // to_coef (one GEMM over all nodes)
   } else if (!plan.s2mTilesHost.empty()) {
     k += plan.options.barnesHut ? 1 : chunks(plan.P);
