@@ -260,8 +260,9 @@ void buildMomentPlan(DevicePlan& plan) {
   uploadVec(plan.dFarNodes, plan.farNodesHost, st);
   // top levels by composite shifts from the depth-m2mTop frontier (moments.cu
   // m2m_pairs): one launch instead of one latency-bound launch per level
-  constexpr int kM2MTopDepth = 6;
-  plan.m2mTop = std::min(kM2MTopDepth, maxDepth);
+  int topDepth = 8;  // B200 sweep 0/6/8/10 (cfg2 S2M 0.294/0.245/0.233/0.248 ms); FKTB_M2M_TOP overrides
+  if (const char* e = std::getenv("FKTB_M2M_TOP")) topDepth = std::max(0, std::atoi(e));
+  plan.m2mTop = std::min(topDepth, maxDepth);
   std::vector<int> topPairs;
   for (int b = 0; b < t.nodes; ++b) {
     if (t.left[static_cast<size_t>(b)] < 0 || depth[static_cast<size_t>(b)] >= plan.m2mTop) continue;

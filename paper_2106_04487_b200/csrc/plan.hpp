@@ -151,7 +151,7 @@ struct DevicePlan {
   std::vector<FktbTile> p2mTilesHost;
   DeviceBuffer<FktbTile> dP2mTiles;
   std::vector<int> levelOff;     // internal nodes grouped by depth: [levelOff[l], levelOff[l+1])
-  // Narrow top of the tree: internal nodes shallower than m2mTop get their
+  // Narrow top of the tree: internal nodes shallower than m2mTop (8) get their
   // moments in ONE launch, straight from their frontier (descendants at depth
   // m2mTop, or leaves above it) by composite shifts; (node, frontier) pairs.
   int m2mTop = 0;
