@@ -307,26 +307,37 @@ __global__ void m2m_pairs(const __grid_constant__ MomArgs A, const int* pairs, i
 
 // Node moments in the FKT basis for every (rhs, node) row: out[R][P] =
 // mono[R][C] * TT[C][P] -- a small GEMM, 32 rows per CTA staged in shared
-// memory, TT columns read coalesced (same for every CTA: L1/L2 resident).
+// memory (even row stride: each thread reads two monomials of a row with one
+// broadcast LDS.128), TT columns read coalesced (L1/L2 resident).
 constexpr int kTcRows = 32;
 __global__ void __launch_bounds__(128) to_coef_gemm(const double* mono, const double* TT, double* out, int R, int C,
                                                    int P) {
-  extern __shared__ double smu[];  // [kTcRows][C + 1]
+  extern __shared__ __align__(16) double smu[];  // [kTcRows][CS], CS = C rounded up to even
+  const int CS = (C + 1) & ~1;
   const int r0 = blockIdx.x * kTcRows;
   const int rows = min(kTcRows, R - r0);
-  for (int i = threadIdx.x; i < rows * C; i += blockDim.x) {
-    const int rr = i / C, a = i % C;
-    smu[rr * (C + 1) + a] = mono[static_cast<size_t>(r0 + rr) * C + a];
+  for (int i = threadIdx.x; i < kTcRows * CS; i += blockDim.x) {
+    const int rr = i / CS, a = i % CS;
+    smu[i] = rr < rows && a < C ? mono[static_cast<size_t>(r0 + rr) * C + a] : 0.0;
   }
   __syncthreads();
   for (int c = threadIdx.x; c < P; c += blockDim.x) {
     double acc[kTcRows];
 #pragma unroll
     for (int i = 0; i < kTcRows; ++i) acc[i] = 0.0;
-    for (int a = 0; a < C; ++a) {
-      const double t = TT[static_cast<size_t>(a) * P + c];
+    int a = 0;
+    for (; a + 1 < C; a += 2) {
+      const double t0 = TT[static_cast<size_t>(a) * P + c], t1 = TT[static_cast<size_t>(a + 1) * P + c];
 #pragma unroll
-      for (int i = 0; i < kTcRows; ++i) acc[i] = fma(t, smu[i * (C + 1) + a], acc[i]);
+      for (int i = 0; i < kTcRows; ++i) {
+        const double2 m = *reinterpret_cast<const double2*>(smu + i * CS + a);
+        acc[i] = fma(t1, m.y, fma(t0, m.x, acc[i]));
+      }
+    }
+    if (a < C) {  // odd C
+      const double t0 = TT[static_cast<size_t>(a) * P + c];
+#pragma unroll
+      for (int i = 0; i < kTcRows; ++i) acc[i] = fma(t0, smu[i * CS + a], acc[i]);
     }
 #pragma unroll
     for (int i = 0; i < kTcRows; ++i)
@@ -525,7 +536,7 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   // K4c: node moments in the FKT basis, every (rhs, node) row at once.
   if (!plan.farNodesHost.empty()) {
     const int R = nrhs * t.nodes;
-    const size_t smem = static_cast<size_t>(kTcRows) * (C + 1) * sizeof(double);
+    const size_t smem = static_cast<size_t>(kTcRows) * ((C + 1) & ~1) * sizeof(double);
     if (smem > 48 * 1024)
       FKTB_CUDA(cudaFuncSetAttribute(to_coef_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     to_coef_gemm<<<(R + kTcRows - 1) / kTcRows, 128, smem, st>>>(plan.dMono.get(), plan.dMomTT.get(), moments, R, C,
