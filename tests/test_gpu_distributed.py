@@ -97,6 +97,20 @@ def test_sharded_multi_rhs(fkt):
     assert np.linalg.norm(z.cpu().numpy() - z1) / np.linalg.norm(z1) <= 1e-13
 
 
+def test_sharded_sixteen_rhs_tensor_core_paths(fkt):
+    # 16 RHS: the RHS-blocked P2M and the FP64 tensor-core M2T under target
+    # shards (re-tiled far / P2M lists), 3 shards summed = unsharded
+    import torch
+
+    x, y = fkt.synthCloud("mixture", 60000, 2, 4)
+    pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel("cauchy", {"sigma": 1.0}),
+                  fkt.FktOptions(p=6, theta=0.75, leafCapacity=512))
+    Y = torch.from_numpy(np.stack([np.roll(y, 7 * r) * (1 + 0.1 * r) for r in range(16)])).cuda().contiguous()
+    z1 = pl.multiply_device(Y).cpu().numpy()
+    z, _ = _simulate(fkt, pl, Y, 3)
+    assert np.linalg.norm(z.cpu().numpy() - z1) / np.linalg.norm(z1) <= 1e-13
+
+
 def test_shards_are_cost_balanced(fkt):
     """Leaf-aligned cuts: the heaviest shard's near+far pair count stays close
     to the mean (the cut rule balances the per-target cost model)."""
