@@ -67,7 +67,7 @@ KERNELS = [
 
 
 @pytest.mark.parametrize("name,params", KERNELS)
-@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("d", [2, 3, 5])
 def test_kernels_small(fkt, ref, name, params, d):
     x, y = fkt.synthCloud("sphere" if d == 3 else "cube", 3000, d, 7)
     opts = fkt.FktOptions(p=4, theta=0.75, leafCapacity=128)
@@ -89,3 +89,19 @@ def test_orders_dims(fkt, ref, d, p, compression):
     rp = ref.RefPlan(x, "gaussian", {}, p=p, theta=0.6, leaf=100, compression=compression)
     assert pl.coefficientCount() == rp.coef
     assert fkt.relativeError(pl.multiply(y), rp.multiply(y)) <= TOL
+
+
+@pytest.mark.parametrize("name,params", KERNELS)
+def test_kernels_sixteen_rhs(fkt, ref, name, params):
+    # 16 right-hand sides through every kernel's multi-RHS paths (RHS-blocked
+    # P2M, tensor-core M2T incl. the runtime-kernel instantiation, 16-RHS
+    # near field): each column against the reference's single-RHS multiply
+    x, y = fkt.synthCloud("sphere", 4000, 3, 9)
+    W = np.stack([np.roll(y, 13 * r) * (1.0 + 0.05 * r) for r in range(16)], axis=1)
+    opts = fkt.FktOptions(p=4, theta=0.75, leafCapacity=128)
+    p = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(name, params), opts)
+    rp = ref.RefPlan(x, name, params, p=4, theta=0.75, leaf=128)
+    Z = p.multiply(W)
+    for c in (0, 5, 15):
+        col = np.ascontiguousarray(W[:, c])
+        assert fkt.relativeError(Z[:, c], rp.multiply(col)) <= TOL, (c,)
