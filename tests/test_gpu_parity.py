@@ -79,7 +79,8 @@ def test_kernels_small(fkt, ref, name, params, d):
     assert fkt.relativeError(z, zr) <= TOL
 
 
-@pytest.mark.parametrize("d,p", [(2, 6), (3, 4), (3, 6), (3, 8), (4, 4), (5, 4), (2, 3), (3, 2), (4, 2), (6, 2)])
+@pytest.mark.parametrize("d,p", [(2, 6), (3, 4), (3, 6), (3, 8), (4, 4), (5, 4), (2, 3), (3, 2), (4, 2), (6, 2),
+                                 (3, 0), (2, 1), (3, 1), (5, 2), (2, 10), (3, 10)])
 @pytest.mark.parametrize("compression", [1, 2])
 def test_orders_dims(fkt, ref, d, p, compression):
     x, y = fkt.synthCloud("mixture", 2500, d, 11)
