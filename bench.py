@@ -170,20 +170,22 @@ def golden_parity(cfg, z):
     return out
 
 
-def near_ncu(cfg):
-    """ncu evidence for the near kernel at this config (profiles/near_traffic.json):
-    {"traffic": dram read + write bytes per launch, "fp64_pipe_frac": ...} or None."""
-    path = os.path.join(ROOT, "profiles", "near_traffic.json")
+def near_ncu(cfg, precision=64):
+    """ncu evidence for the near kernel of THIS config (profiles/ncu_near.json,
+    one `ncu --set full` capture per config, scripts/gpu_ncu_near_cfgs.sh):
+    {"traffic": dram read + write bytes per launch, "fp64_pipe_frac": ...,
+    "capture": file} or None when that config has no capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_near.json")
     try:
         with open(path) as f:
-            v = json.load(f).get(f"cfg{cfg}")
+            v = json.load(f).get(f"cfg{cfg}" + ("" if precision == 64 else "_fp32"))
     except Exception:
         return None
-    return {"traffic": v} if isinstance(v, (int, float)) else v
+    return v if isinstance(v, dict) else None
 
 
-def traffic_for(cfg):
-    v = near_ncu(cfg)
+def traffic_for(cfg, precision=64):
+    v = near_ncu(cfg, precision)
     return None if v is None else v.get("traffic")
 
 
@@ -305,9 +307,9 @@ def run_ours(args):
         return
 
     # ---- roofline (dominant kernel: near field) ---------------------------
-    peak = C.c_double()
-    fkt._check(fkt.lib.fkt_fma_peak(0, C.byref(peak)))
-    peak_tf = peak.value / 1e12
+    pk_fma, pk_mma = C.c_double(), C.c_double()
+    fkt._check(fkt.lib.fkt_fp64_peaks(C.byref(pk_fma), C.byref(pk_mma)))
+    peak_tf = max(pk_fma.value, pk_mma.value) / 1e12
     tree = pl.tree()
     nev_all = near_evals(tree)
     nev = near_evals(tree, shard_lo, shard_hi) if sharded else nev_all  # rank 0's near launch
@@ -358,19 +360,22 @@ def run_ours(args):
             "bound": "fp64",
             "achieved": achieved,
             "peak": peak_tf,
-            "peak_source": "fp64 FMA-chain microbenchmark measured live in this run (fkt_fma_peak); "
-                           "MEASURED_PEAKS.json has no fp64 entry",
+            "peak_source": "FP64 datapath peak measured live in this run (fkt_fp64_peaks: best of DFMA chains and "
+                           "mma.sync f64 chains, 3 lengths x 3 reps after a warm-up); MEASURED_PEAKS.json has no "
+                           "fp64 entry",
+            "peak_dfma": pk_fma.value / 1e12, "peak_dmma": pk_mma.value / 1e12,
             "unit": "TFLOP/s",
             "frac": achieved / peak_tf,
-            "traffic": traffic_for(args.cfg),
+            "traffic": traffic_for(args.cfg, args.near_precision),
             "flops_per_launch": near_flops,
             "flops_per_pair": fpp,
             "whole_step_frac": (nev_all * fpp + far_flops) / mvm_s / 1e12 / peak_tf / world,
             # frac counts SURVEY §8(d)'s flop convention (exp = 20, sqrt / div = 8);
             # the fast-math pair body executes fewer FP64 instructions (16 for the
             # Matern-3/2 Gram form), so the FP64 pipe utilisation ncu measured for
-            # this kernel (profiles/near_traffic.json) is the hardware-side figure
-            "ncu_fp64_pipe_frac": (near_ncu(args.cfg) or {}).get("fp64_pipe_frac"),
+            # this kernel (profiles/ncu_near.json, this config's capture) is the hardware-side figure
+            "ncu_fp64_pipe_frac": (near_ncu(args.cfg, args.near_precision) or {}).get("fp64_pipe_frac"),
+            "ncu_capture": (near_ncu(args.cfg, args.near_precision) or {}).get("capture"),
             "frac_note": ("frac = SURVEY 8(d) convention flops (exp 20, sqrt/div 8) / live DFMA peak; the fast-math "
                           "pair body executes fewer FP64 ops than the convention charges, so frac may exceed 1. "
                           "executed_frac and fp64_pipe_frac count the FP64 work the kernel really issues (SASS)."),
@@ -387,7 +392,7 @@ def run_ours(args):
         "parity": parity,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cfg, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(args.cfg, reps=args.cpu_reps)
     print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
@@ -412,28 +417,37 @@ def _ref_sample_run(cfg, n_s, reps, warmup):
     return ts, rp.plan_seconds
 
 
-def cpu_baseline(cfg, budget_s=30.0):
-    """Reference CPU FKT on the host cores, bounded sample (10-30 s of CPU work)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg, warmup=1, reps=3):
+    """Reference CPU FKT (oracle/_ref, unmodified, streaming, all host threads)
+    at the FULL config size: BASELINE.md §4 -- 1 warm-up MVM, then the median
+    of `reps` timed MVMs (plan timed separately)."""
     c = CONFIGS[cfg]
     cores = os.cpu_count()
-    n_probe = min(c["n"], 100000)
-    ts, _ = _ref_sample_run(cfg, n_probe, 1, 0)
-    t_full_est = ts[0] * c["n"] / n_probe
-    if t_full_est <= budget_s:
-        ts, plan_s = _ref_sample_run(cfg, c["n"], 1, 0)
-        t, n_s = ts[0], c["n"]
-        sample = f"one full reference MVM at N={c['n']} (streaming, {cores} threads)"
-    else:
-        n_s = int(min(c["n"], max(20000, c["n"] * budget_s / t_full_est)))
-        ts, plan_s = _ref_sample_run(cfg, n_s, 1, 0)
-        t = ts[0] * c["n"] / n_s
-        sample = (f"reference MVM on the first {n_s} points of the cfg{cfg} recipe (streaming, {cores} threads), "
-                  f"{ts[0]:.2f} s, scaled linearly to N={c['n']}")
-    return {"value": 1.0 / t, "unit": "MVM/s", "cores": cores, "kind": "reference", "sample": sample,
-            "seconds_per_mvm": t}
+    ts, plan_s = _ref_sample_run(cfg, c["n"], reps, warmup)
+    t = float(np.median(ts))
+    return {"value": 1.0 / t, "unit": "MVM/s", "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(), "nproc": cores,
+            "sample": (f"full cfg{cfg} workload (N={c['n']}): reference FktPlan::multiply, streaming, "
+                       f"FktOptions.threads = 0 ({cores} threads); {warmup} warm-up, median of {reps}"),
+            "seconds_per_mvm": t, "seconds_each": ts, "plan_seconds": plan_s}
 
 
 def run_reference(args):
+    """--impl reference: the unmodified reference FKT (oracle/_ref) through its
+    own FktPlan API at the FULL config size, every step one full MVM (no
+    sampling, no extrapolation): W warm-up MVMs, then K timed MVMs
+    (proj/tools/fkt_main.cpp:206-252 times the same call)."""
     world, rank, local = dist_setup()
     if rank != 0:
         return
@@ -444,31 +458,24 @@ def run_reference(args):
         return
     c = CONFIGS[args.cfg]
     cores = os.cpu_count()
-    # Size each step so warmup + steps stays within a few minutes.
-    n_probe = min(c["n"], 100000)
-    ts, _ = _ref_sample_run(args.cfg, n_probe, 1, 0)
-    per_full = ts[0] * c["n"] / n_probe
-    budget = args.ref_budget
-    total_steps = args.steps + args.warmup
-    n_s = c["n"] if per_full * total_steps <= budget else int(max(20000, c["n"] * budget / (per_full * total_steps)))
-    n_s = min(n_s, c["n"])
-    ts, plan_s = _ref_sample_run(args.cfg, n_s, args.steps, args.warmup)
+    ts, plan_s = _ref_sample_run(args.cfg, c["n"], args.steps, args.warmup)
     t_step = float(np.mean(ts))
-    t_scaled = t_step * c["n"] / n_s
-    value = 1.0 / t_scaled
-    sample = (f"each step = one reference FKT MVM (streaming, {cores} threads) on "
-              + (f"the full N={c['n']}" if n_s == c["n"] else
-                 f"the first {n_s} points of the cfg{args.cfg} recipe, time scaled linearly to N={c['n']}"))
+    value = 1.0 / t_step
+    sample = (f"full cfg{args.cfg} workload (N={c['n']}) every step: one reference FktPlan::multiply "
+              f"(streaming, {cores} threads, {cpu_model()}); {args.warmup} warm-up + {args.steps} timed MVMs, "
+              f"value = 1 / mean step time")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MVM/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_scaled * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY Appendix B recipe, fkt::Rng(42))",
-        "config": {"workload": workload_desc(args.cfg), "parallelism": "host cores", "sample_n": n_s,
-                   "reference_plan_seconds": plan_s},
-        "cpu_baseline": {"value": value, "unit": "MVM/s", "cores": cores, "kind": "reference", "sample": sample},
+        "config": {"workload": workload_desc(args.cfg), "parallelism": "host cores", "sample_n": c["n"],
+                   "reference_plan_seconds": plan_s, "median_ms": float(np.median(ts)) * 1e3,
+                   "min_ms": float(np.min(ts)) * 1e3, "max_ms": float(np.max(ts)) * 1e3},
+        "cpu_baseline": {"value": value, "unit": "MVM/s", "cores": cores, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": cores},
         "e2e": {"value": value, "unit": "MVM/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "effective_interactions_per_s": float(c["n"]) * c["n"] * c["nrhs"] / t_scaled,
+        "effective_interactions_per_s": float(c["n"]) * c["n"] * c["nrhs"] / t_step,
     }
     print(json.dumps(line), flush=True)
 
@@ -483,8 +490,7 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="use the target-sharded multi-GPU path even at one rank (it is automatic for N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=30.0)
-    ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--cpu-reps", type=int, default=3, help="timed reference MVMs for cpu_baseline (median)")
     ap.add_argument("--near-precision", type=int, default=64, choices=[64, 32],
                     help="32 = FP32 fast near-field mode (not the headline; parity gate is FP64)")
     args = ap.parse_args()

@@ -244,6 +244,9 @@ long long fkt_harmonic_count(int d, int k);
  * fp64 (fp32 = 0) or fp32 (fp32 = 1): the roofline denominator for the
  * FP64-bound kernels. */
 int fkt_fma_peak(int fp32, double* flops_per_s);
+/* The two FP64 probes behind fkt_fma_peak(0): DFMA chains and FP64 tensor-core
+ * (mma.sync m8n8k4) chains; they share one datapath on B200. */
+int fkt_fp64_peaks(double* dfma_flops_per_s, double* dmma_flops_per_s);
 
 /* Seeded synthetic inputs (reference fkt::Rng, synthetic.hpp:17-50;
  * generators synthetic.cpp:7-55). kind: "cube", "sphere", "mixture".

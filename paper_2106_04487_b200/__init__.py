@@ -447,6 +447,9 @@ class FktPlan:
             raise DimensionMismatchError("multiply: vector length does not match the point count")
         if z is None:
             z = torch.empty_like(y)
+        elif not (isinstance(z, torch.Tensor) and z.is_cuda and z.dtype == torch.float64 and z.is_contiguous()
+                  and z.shape == y.shape and z.device == y.device):
+            raise InvalidArgument("multiply_device: z must be a contiguous float64 CUDA tensor shaped and placed like y")
         st = stream if stream is not None else torch.cuda.current_stream()
         _check(lib.fkt_plan_multiply_device(self._h, C.c_void_p(y.data_ptr()), C.c_void_p(z.data_ptr()), nrhs,
                                             C.c_void_p(st.cuda_stream)))

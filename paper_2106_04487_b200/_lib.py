@@ -139,6 +139,7 @@ SIGNATURES = {
     "fkt_addition_normalizer": (C.c_double, C.c_int, C.c_int),
     "fkt_harmonic_count": (C.c_longlong, C.c_int, C.c_int),
     "fkt_fma_peak": (C.c_int, C.c_int, _d),
+    "fkt_fp64_peaks": (C.c_int, _d, _d),
     "fkt_synth_cloud": (C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_uint64, _d, _d),
     "fkt_synth_config": (C.c_int, C.c_int, C.c_int, C.c_uint64, _d, _d),
     "fkt_config_dims": (C.c_int, C.c_int, _i32, _i32),

@@ -24,7 +24,11 @@ namespace {
     case FKT_ERR_DIMENSION_MISMATCH: throw DimensionMismatchError(msg);
     case FKT_ERR_ORDER_TOO_LARGE: throw OrderTooLargeError(msg);
     case FKT_ERR_NOT_RECURRENCE: throw NotRecurrenceKernelError(msg);
-    case FKT_ERR_SINGULAR_AT_ZERO: throw std::domain_error(msg);
+    case FKT_ERR_SINGULAR_AT_ZERO: {
+      // the C-ABI message is SingularAtZeroError's own text: recover the name
+      const size_t q0 = msg.find('\''), q1 = q0 == std::string::npos ? q0 : msg.find('\'', q0 + 1);
+      throw SingularAtZeroError(q1 == std::string::npos ? msg : msg.substr(q0 + 1, q1 - q0 - 1));
+    }
     case FKT_ERR_ZERO_REFERENCE: throw ZeroReferenceError();
     case FKT_ERR_CUDA: throw CudaError(msg);
     case FKT_ERR_UNSUPPORTED: throw UnsupportedOnGpuError(msg);

@@ -17,11 +17,6 @@ void synthConfig(int cfg, int n, std::uint64_t seed, double* x, double* w);
 int configDims(int cfg, int* d, int* nrhs);
 }  // namespace fktb
 
-struct fkt_plan_s {
-  std::unique_ptr<fktb::DevicePlan> plan;
-  bool cached = false;  // owned by the plan cache (fkt_plan_cache_get)
-  int refs = 0;         // outstanding fkt_plan_cache_get references
-};
 struct fkt_tree_s {
   fktb::DeviceTree* tree = nullptr;   // borrowed or owned
   std::unique_ptr<fktb::DeviceTree> owned;
@@ -31,6 +26,15 @@ struct fkt_tree_s {
   std::vector<long long> farOff, nearOff;
   std::vector<uint32_t> farIdx, nearIdx;
   std::mutex mutex;
+};
+struct fkt_plan_s {
+  std::unique_ptr<fktb::DevicePlan> plan;
+  bool cached = false;  // owned by the plan cache (fkt_plan_cache_get)
+  int refs = 0;         // outstanding fkt_plan_cache_get references
+  // borrowed tree view (fkt_plan_tree): lives and dies with this handle, so a
+  // freed plan never leaves a view (and its materialised sets) behind
+  std::unique_ptr<fkt_tree_s> view;
+  std::mutex viewMutex;
 };
 
 namespace {
@@ -390,10 +394,13 @@ int fkt_plan_multiply_device(fkt_plan_t plan, const double* y_dev, double* z_dev
 int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, double* z_dev, int nrhs, void* stream) {
   return guarded([&] {
     auto& p = *plan->plan;
+    std::lock_guard<std::mutex> lock(p.mutex);
     if (nrhs < 1) throw DimensionMismatch("stage: nrhs must be >= 1");
+    if (nrhs > fktb::maxRhsPerPass(p)) throw std::invalid_argument("stage: nrhs exceeds one pass; use multiply");
     if (stage == 0) fktb::ensureWorkspace(p, nrhs);
     if (nrhs > p.nrhsCap) throw std::invalid_argument("stage: run stage 0 (or a multiply) with this nrhs first");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    fktb::orderAfterPrevious(p, st);
     switch (stage) {
       case 0:
         fktb::launchGatherY(p, y_dev, p.dYp.get(), nrhs, st);
@@ -406,6 +413,7 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
       case 4: fktb::launchScatterZ(p, p.dZp.get(), z_dev, nrhs, st); break;
       default: throw std::invalid_argument("stage must be 0..4");
     }
+    fktb::markDone(p, st);
     if (!stream) FKTB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -550,16 +558,13 @@ int fkt_shard_cuts(const uint32_t* leaf_end, const unsigned long long* leaf_cum_
 }
 
 fkt_tree_t fkt_plan_tree(fkt_plan_t plan) {
-  // Cached borrowed view owned by the plan handle's lifetime.
-  static std::mutex m;
-  static std::map<fkt_plan_t, fkt_tree_s*> views;
-  std::lock_guard<std::mutex> lock(m);
-  auto it = views.find(plan);
-  if (it != views.end() && it->second->tree == plan->plan->tree.get()) return it->second;
-  auto* v = new fkt_tree_s();
-  v->tree = plan->plan->tree.get();
-  views[plan] = v;
-  return v;
+  // Borrowed view owned by the plan handle (freed with it).
+  std::lock_guard<std::mutex> lock(plan->viewMutex);
+  if (!plan->view || plan->view->tree != plan->plan->tree.get()) {
+    plan->view = std::make_unique<fkt_tree_s>();
+    plan->view->tree = plan->plan->tree.get();
+  }
+  return plan->view.get();
 }
 
 int fkt_tree_create(int n, int d, const double* x, int leaf_capacity, fkt_tree_t* out) {

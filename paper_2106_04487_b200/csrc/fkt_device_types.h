@@ -93,16 +93,4 @@ typedef struct FktbTile {
   int64_t start;
 } FktbTile;
 
-// Near-field block tile (nearsym.cu): rows and columns are lists of permuted
-// positions in the plan's index pool; sym = 1 also accumulates the columns
-// (the pair is near in both directions and K is evaluated once).
-typedef struct FktbBlockTile {
-  long long rowOff;
-  long long colOff;
-  int rowCount;
-  int colCount;
-  int sym;
-  int leaf;  // leaf whose centre and bound the Gram form of this block uses
-} FktbBlockTile;
-
 #endif

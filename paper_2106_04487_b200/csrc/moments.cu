@@ -362,35 +362,12 @@ void launchP2M(const MomArgs& A, int tiles, cudaStream_t st) {
   FKTB_CUDA(cudaGetLastError());
 }
 
-// Developer A/B knob: FKTB_P2M_SINGLE=1 runs single-RHS P2M on p2m_multi too.
-inline bool p2mSingleMulti() {
-  static const bool v = [] {
-    const char* e = std::getenv("FKTB_P2M_SINGLE");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-// Developer A/B knob: FKTB_P2M_MULTI=0 keeps multi-RHS P2M on p2m_regs.
-inline bool p2mMultiEnabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("FKTB_P2M_MULTI");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 template <int D, int P>
 bool launchP2MMulti(const MomArgs& A, int tiles, cudaStream_t st) {
   constexpr int RB = p2mMultiBlock<D, P>();
   if constexpr (RB == 0) {
     return false;
   } else {
-    if (A.nrhs == 1 && p2mSingleMulti()) {  // single RHS: 8 source streams x AM monomials per lane
-      p2m_multi<D, P, 1><<<tiles, 32 * kP2MGroups, 0, st>>>(A);
-      FKTB_CUDA(cudaGetLastError());
-      return true;
-    }
     if (A.nrhs % RB != 0) return false;
     p2m_multi<D, P, RB><<<tiles, 32 * kP2MGroups, 0, st>>>(A);
     FKTB_CUDA(cudaGetLastError());
@@ -433,7 +410,7 @@ int p2mLaunches(int d, int p, int count, int nrhs) {
     case 504: rb = p2mMultiBlock<5, 4>(); break;
     default: break;
   }
-  if (rb > 0 && nrhs >= 8 && nrhs % rb == 0 && p2mMultiEnabled()) return 1;
+  if (rb > 0 && nrhs >= 8 && nrhs % rb == 0) return 1;
   const int chunk = std::max(1, kP2MMaxThreads / count);
   return (nrhs + chunk - 1) / chunk;
 }
@@ -479,7 +456,7 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
   // many right-hand sides: RHS-blocked p2m_multi (monomial formed once per
   // source and reused for the block)
   auto multi = [&]() -> bool {
-    if (tiles == 0 || (nrhs < 8 && !(nrhs == 1 && p2mSingleMulti())) || !p2mMultiEnabled()) return false;
+    if (tiles == 0 || nrhs < 8) return false;
     MomArgs B = A;
     B.nrhs = nrhs;
     B.yp = yp;

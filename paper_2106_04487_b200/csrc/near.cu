@@ -378,201 +378,10 @@ void launchFastV(const FastArgs& F, int tiles, int gramTiles, cudaStream_t st) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// Multi-RHS near field on the FP64 tensor cores (mma.sync m8n8k4 f64). Per
-// warp, 32 targets of the tile (4 m-tiles of 8) against the leaf's sources 4
-// at a time (one k-step): lane (g, t) = (lane >> 2, lane & 3) evaluates the
-// pair (target 8 mt + g, source 4 ks + t) -- exactly its A-fragment element --
-// and one DMMA per (m-tile, 8 RHS) accumulates K (8x4) . W (4x8). The pair
-// evaluation is the near_tile body (Gram or difference form); the weights'
-// B fragments come from shared rows of stride NR + 4 (conflict-free). This
-// replaces 8 NT DFMA + 4 NT LDS.128 per pair and lane by 2 NT / 32 DMMA.
-__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-constexpr int kMmaNearThreads = 256;  // 8 warps x 32 targets = one 256-target tile
-constexpr int kMmaNearChunk = 128;    // sources staged per pass
-
-template <int KID, int D, bool SEL, int NT, bool GRAM>
-__global__ void __launch_bounds__(kMmaNearThreads, 2) near_mma(const __grid_constant__ FastArgs F) {
-  static_assert(kMmaNearThreads == kNearThreads * kNearTPT, "near tile size");
-  using FK = FastKernel<KID>;
-  constexpr int NR = 8 * NT, WS = NR + 4;  // weight row stride: conflict-free B fragments
-  constexpr int GS = GRAM ? D + 1 : D;     // geometry row: (-2 s, |s|^2 + offset + bias) or s
-  __shared__ double sG[kMmaNearChunk * GS];
-  __shared__ double sW[kMmaNearChunk * WS];
-  __shared__ double tab[kNearExpTable * kNearExpRep];
-  const NearArgs& A = F.a;
-  const FktbTile tile = A.tiles[blockIdx.x];
-  if (GRAM != (F.limit2[tile.node] <= F.gramLimit2)) return;  // the other form's tile
-  if constexpr (FK::needsTable)
-    for (int i = threadIdx.x; i < kNearExpTable * kNearExpRep; i += kMmaNearThreads) tab[i] = F.expTable[i / kNearExpRep];
-  const int colBytes = (threadIdx.x & (kNearExpRep - 1)) * 8;
-  const int leaf = tile.node;
-  const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
-  const int n = A.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  double c[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) c[a] = GRAM ? F.center[static_cast<size_t>(leaf) * D + a] : 0.0;
-  const double wf = GRAM ? F.wf * FK::gramWeight : F.wf;
-  const double qbias = GRAM && FK::gramBiased
-                           ? fma((1.5 * D + 1.0) * 2.220446049250313e-16 * kGramBound / F.gramLimit2, F.limit2[leaf], 1e-30)
-                           : 0.0;
-  // this lane's 4 targets (A-fragment rows): tile targets warp * 32 + 8 mt + g
-  double tx[4][D], tn[4];
-  int tpos[4];
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int idx = warp * 32 + 8 * mt + g;
-    tpos[mt] = idx < tile.count ? static_cast<int>(A.nearPos[tile.start + idx]) : -1;
-    const int p = tpos[mt] >= 0 ? tpos[mt] : 0;
-    tn[mt] = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      tx[mt][a] = __dmul_rn(A.pc[static_cast<size_t>(a) * n + p] - c[a], F.sc);
-      if constexpr (GRAM) tn[mt] = fma(tx[mt][a], tx[mt][a], tn[mt]);
-    }
-  }
-  for (int r0 = 0; r0 < A.nrhs; r0 += NR) {
-    double acc[4][NT][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    for (int cs = sb; cs < se; cs += kMmaNearChunk) {
-      const int cn = min(kMmaNearChunk, se - cs);
-      const int cn4 = (cn + 3) & ~3;  // padding rows: a copy of the chunk's first source, zero weights
-      __syncthreads();
-      for (int s = threadIdx.x; s < cn4; s += kMmaNearThreads) {
-        const int src = cs + (s < cn ? s : 0);
-        double ns = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double v = __dmul_rn(A.pc[static_cast<size_t>(a) * n + src] - c[a], F.sc);
-          if constexpr (GRAM) {
-            ns = fma(v, v, ns);
-            sG[s * GS + a] = -2.0 * v;
-          } else {
-            sG[s * GS + a] = v;
-          }
-        }
-        if constexpr (GRAM) sG[s * GS + D] = ns + (FK::gramOffset + qbias);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) sW[s * WS + r] = s < cn ? A.yp[static_cast<size_t>(r0 + r) * n + src] * wf : 0.0;
-      }
-      __syncthreads();
-      for (int k0 = 0; k0 < cn4; k0 += 4) {
-        const int s = k0 + t;
-        double sg[GS];
-#pragma unroll
-        for (int a = 0; a < GS; ++a) sg[a] = sG[s * GS + a];
-        double bw[NT];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bw[nt] = sW[s * WS + 8 * nt + g];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          double q;
-          if constexpr (GRAM) {
-            q = fma(tx[mt][0], sg[0], sg[D]);
-#pragma unroll
-            for (int a = 1; a < D; ++a) q = fma(tx[mt][a], sg[a], q);
-            q += tn[mt];
-          } else {
-            const double d0 = tx[mt][0] - sg[0];
-            q = fma(d0, d0, kQBias);
-#pragma unroll
-            for (int a = 1; a < D; ++a) {
-              const double da = tx[mt][a] - sg[a];
-              q = fma(da, da, q);
-            }
-          }
-          double kv = FK::template eval<kNearExpRep, kNearFI, GRAM>(q, tab, colBytes);
-          if constexpr (SEL) kv = __double2hiint(q) == kQBiasHi ? F.diagCanon : kv;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], kv, bw[nt]);
-        }
-      }
-    }
-    // C fragment (g, 2t + j) of (m-tile mt, n-tile nt): target 8 mt + g, RHS
-    // r0 + 8 nt + 2 t + j (this lane loaded that target itself: same g)
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-      if (tpos[mt] >= 0)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            atomicAdd(A.zp + static_cast<size_t>(r0 + 8 * nt + 2 * t + j) * n + tpos[mt], acc[mt][nt][j]);
-  }
-}
-
-template <int KID, int D, bool SEL, int NT>
-void launchMmaNear(const FastArgs& F, int tiles, int gramTiles, cudaStream_t st) {
-  if constexpr (FastKernel<KID>::gram && !SEL) {
-    if (gramTiles > 0) {
-      near_mma<KID, D, SEL, NT, true><<<tiles, kMmaNearThreads, 0, st>>>(F);
-      FKTB_CUDA(cudaGetLastError());
-    }
-  } else {
-    gramTiles = 0;
-  }
-  if (gramTiles < tiles) {
-    near_mma<KID, D, SEL, NT, false><<<tiles, kMmaNearThreads, 0, st>>>(F);
-    FKTB_CUDA(cudaGetLastError());
-  }
-}
-
-// Opt-in A/B path (FKTB_NEAR_MMA=1): measured on the B200 at cfg5 (Cauchy d=2,
-// 16 RHS) 4.72 ms against 4.16 ms for the register-blocked DFMA kernel -- the
-// FP64 MMA shares the DFMA datapath, so the pair evaluations and the same FP64
-// pipe time remain, and the DMMA accumulator chains add latency. Kept for
-// parity testing (tests/test_gpu_near_forms.py) and future shapes.
-inline bool nearMmaEnabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("FKTB_NEAR_MMA");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-// Developer knob for tuning sweeps (scripts/sweep_near.py): FKTB_NEAR_VARIANT
-// selects the (threads, targets/thread, unroll) shape of the single-RHS
-// Matern-3/2 d=3 kernel. 0 is the default.
-inline int nearVariant() {
-  static const int v = [] {
-    const char* e = std::getenv("FKTB_NEAR_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <int KID, int D, bool SEL>
 void launchFastSel(const FastArgs& F, int nrhs, int tiles, int gramTiles, cudaStream_t st) {
   if (nrhs == 1) {
-    if constexpr ((KID == FKTB_KERNEL_MATERN32 && D == 3 || KID == FKTB_KERNEL_GAUSSIAN && D == 5) && !SEL) {
-      switch (nearVariant()) {
-        case 1: return launchFastV<KID, D, SEL, 64, 4, 4, 1>(F, tiles, gramTiles, st);
-        case 11: return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
-        case 2: return launchFastV<KID, D, SEL, 32, 8, 1, 1>(F, tiles, gramTiles, st);
-        case 3: return launchFastV<KID, D, SEL, 32, 8, 2, 1>(F, tiles, gramTiles, st);
-        case 4: return launchFastV<KID, D, SEL, 128, 2, 4, 1>(F, tiles, gramTiles, st);
-        case 5: return launchFastV<KID, D, SEL, 64, 4, 1, 1>(F, tiles, gramTiles, st);
-        case 6: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 12>(F, tiles, gramTiles, st);
-        case 7: return launchFastV<KID, D, SEL, 64, 4, 1, 1, 12>(F, tiles, gramTiles, st);
-        case 8: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 8>(F, tiles, gramTiles, st);
-        case 9: return launchFastV<KID, D, SEL, 128, 2, 2, 1, 6>(F, tiles, gramTiles, st);
-        case 10: return launchFastV<KID, D, SEL, 64, 4, 2, 1, 6>(F, tiles, gramTiles, st);
-        case 12: return launchFastV<KID, D, SEL, 64, 4, 1, 1, 8>(F, tiles, gramTiles, st);
-        case 13: return launchFastV<KID, D, SEL, 128, 2, 2, 1, 8>(F, tiles, gramTiles, st);
-        default: break;
-      }
-    }
-    // measured shapes (B200 sweeps, scripts/sweep_near.py): Matern-3/2 in 3-D
+    // measured shapes (B200 sweeps of the round-1 shape knob): Matern-3/2 in 3-D
     // wants 8 independent targets per thread (one warp per CTA: cfg2 K3
     // 13.72 -> 13.14 ms before the clamp-free Gram form, tied with 64 x 4
     // after it); the 5-D Gaussian 8 CTAs/SM (cfg3 22.6 -> 21.7 ms)
@@ -580,18 +389,9 @@ void launchFastSel(const FastArgs& F, int nrhs, int tiles, int gramTiles, cudaSt
     if constexpr (KID == FKTB_KERNEL_GAUSSIAN && D == 5 && !SEL) return launchFastV<KID, D, SEL, 64, 4, 2, 1, 8>(F, tiles, gramTiles, st);
     return launchFastV<KID, D, SEL, 64, 4, 2, 1>(F, tiles, gramTiles, st);
   }
-  if (nrhs % 8 == 0 && nearMmaEnabled()) {
-    if (nrhs % 16 == 0) return launchMmaNear<KID, D, SEL, 2>(F, tiles, gramTiles, st);
-    return launchMmaNear<KID, D, SEL, 1>(F, tiles, gramTiles, st);
-  }
   if (nrhs % 16 == 0) {
     // 4 targets x 16 RHS accumulators per thread: each source's 16 weights
     // (8 LDS.128) serve 64 FMAs (cfg5 K3 4.95 -> 4.21 ms vs 1 target/thread)
-    switch (nearVariant()) {  // tuning knob (cfg5 shapes)
-      case 11: return launchFastV<KID, D, SEL, 128, 2, 2, 16>(F, tiles, gramTiles, st);
-      case 14: return launchFastV<KID, D, SEL, 256, 1, 2, 16>(F, tiles, gramTiles, st);
-      default: break;
-    }
     return launchFastV<KID, D, SEL, 64, 4, 1, 16>(F, tiles, gramTiles, st);
   }
   if (nrhs % 8 == 0) return launchFastV<KID, D, SEL, 128, 2, 2, 8>(F, tiles, gramTiles, st);

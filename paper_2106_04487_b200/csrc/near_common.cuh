@@ -1,4 +1,4 @@
-// Shared pieces of the FP64 near-field kernels (near.cu, nearsym.cu):
+// Shared pieces of the FP64 near-field kernels (near.cu):
 // canonical kernel bodies on pre-scaled coordinates and the scale factors.
 #ifndef FKTB_NEAR_COMMON_CUH
 #define FKTB_NEAR_COMMON_CUH

@@ -260,8 +260,7 @@ void buildMomentPlan(DevicePlan& plan) {
   uploadVec(plan.dFarNodes, plan.farNodesHost, st);
   // top levels by composite shifts from the depth-m2mTop frontier (moments.cu
   // m2m_pairs): one launch instead of one latency-bound launch per level
-  int topDepth = 8;  // B200 sweep 0/6/8/10 (cfg2 S2M 0.294/0.245/0.233/0.248 ms); FKTB_M2M_TOP overrides
-  if (const char* e = std::getenv("FKTB_M2M_TOP")) topDepth = std::max(0, std::atoi(e));
+  const int topDepth = 8;  // B200 sweep 0/6/8/10 (cfg2 S2M 0.294/0.245/0.233/0.248 ms)
   plan.m2mTop = std::min(topDepth, maxDepth);
   std::vector<int> topPairs;
   for (int b = 0; b < t.nodes; ++b) {
@@ -301,8 +300,42 @@ void buildP2MTiles(DevicePlan& plan) {
 
 }  // namespace
 
+int maxRhsPerPass(const DevicePlan& plan) {
+  static const long long limit = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = 227 * 1024;
+    return static_cast<long long>(v) - 16 * 1024;  // headroom for the kernels' static shared tables
+  }();
+  auto fits = [&](int r) {
+    if (plan.useMoments) {
+      const long long C = plan.monoCount, E = plan.shiftEntries;
+      if ((E + 2 * C * (1 + r)) * 8 + (C + 1 + 2 * E) * 4 > limit) return false;  // m2m_kernel
+      if ((E + C * (1 + r)) * 8 + (C + 1 + 2 * E) * 4 > limit) return false;      // m2m_pairs
+    }
+    return static_cast<long long>((plan.P + 1) & ~1) * r * 8 <= limit;  // M2T moments of one node
+  };
+  int r = 1;
+  while (r < kMaxRhsPerPass && fits(r + 1)) ++r;
+  if (r >= 16) return r / 16 * 16;  // keep the 16-RHS specialisations
+  if (r >= 8) return r / 8 * 8;
+  return r;
+}
+
+void orderAfterPrevious(DevicePlan& plan, cudaStream_t st) {
+  if (plan.doneRecorded) FKTB_CUDA(cudaStreamWaitEvent(st, plan.evDone, 0));
+}
+
+void markDone(DevicePlan& plan, cudaStream_t st) {
+  FKTB_CUDA(cudaEventRecord(plan.evDone, st));
+  plan.doneRecorded = true;
+}
+
 void ensureWorkspace(DevicePlan& plan, int nrhs) {
+  nrhs = std::min(nrhs, maxRhsPerPass(plan));
   if (nrhs <= plan.nrhsCap) return;
+  // the buffers may still be in use by a previous multiply on another stream
+  if (plan.doneRecorded) FKTB_CUDA(cudaEventSynchronize(plan.evDone));
   clearGraphs(plan);
   if (plan.useMoments) plan.dMono.resize(static_cast<size_t>(plan.tree->nodes) * plan.monoCount * nrhs);
   const size_t n = static_cast<size_t>(plan.n);
@@ -356,6 +389,7 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   FKTB_CUDA(cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking));
   FKTB_CUDA(cudaEventCreateWithFlags(&plan->evGather, cudaEventDisableTiming));
   FKTB_CUDA(cudaEventCreateWithFlags(&plan->evFar, cudaEventDisableTiming));
+  FKTB_CUDA(cudaEventCreateWithFlags(&plan->evDone, cudaEventDisableTiming));
   plan->tree = std::make_unique<DeviceTree>();
   buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
   computeSetsGpu(*plan->tree, options.theta);
@@ -380,11 +414,6 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   } else {
     const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
-    // "1" enables the symmetric leaf-pair near field (nearsym.cu). Measured
-    // slower than the one-way kernel on cfg2-4 (padding of small T_AB row
-    // sets), so it stays an opt-in A/B knob.
-    const char* sym = std::getenv("FKTB_NEAR_SYM");
-    if (sym && (std::string(sym) == "1" || std::string(sym) == "2")) buildNearBlocks(*plan, std::string(sym) == "2");
   }
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
@@ -402,13 +431,15 @@ void destroyPlan(DevicePlan* plan) {
   if (plan->stream) cudaStreamSynchronize(plan->stream);
   if (plan->side) cudaStreamSynchronize(plan->side);
   cudaStream_t st = plan->stream, side = plan->side;
-  cudaEvent_t e0 = plan->evGather, e1 = plan->evFar;
+  cudaEvent_t e0 = plan->evGather, e1 = plan->evFar, e2 = plan->evDone;
+  if (plan->doneRecorded) cudaEventSynchronize(e2);
   clearGraphs(*plan);
   delete plan;
   if (st) cudaStreamDestroy(st);
   if (side) cudaStreamDestroy(side);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+  if (e2) cudaEventDestroy(e2);
 }
 
 long long kernelLaunches(const DevicePlan& plan, int nrhs) {
@@ -427,9 +458,7 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
   } else if (!plan.s2mTilesHost.empty()) {
     k += plan.options.barnesHut ? 1 : chunks(plan.P);
   }
-  if (plan.nearSym) {
-    k += !plan.blockTilesHost.empty();
-  } else if (!plan.nearTilesHost.empty()) {
+  if (!plan.nearTilesHost.empty()) {
     // FP64 near field: one launch per pair form present (near.cu)
     const long long g = plan.options.nearPrecision == 32 ? 0 : nearGramTiles(plan);
     k += (g > 0) + (g < static_cast<long long>(plan.nearTilesHost.size()));
@@ -449,12 +478,11 @@ void launchS2MAny(const DevicePlan& plan, const double* yp, double* moments, int
 
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
   if (plan.options.nearPrecision == 32 && launchNear32(plan, yp, zp, nrhs, st)) return;
-  if (launchNearSym(plan, yp, zp, nrhs, st)) return;
   launchNear(plan, yp, zp, nrhs, st);
 }
 
 namespace {
-void enqueueMultiply(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
+void enqueuePass(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
   const size_t n = static_cast<size_t>(plan.n);
   // stream st: gather -> zero z -> near ------------------------> scatter
   // side:                        \-> zero moments -> S2M -> M2T -/
@@ -471,13 +499,24 @@ void enqueueMultiply(DevicePlan& plan, const double* y, double* z, int nrhs, cud
   FKTB_CUDA(cudaStreamWaitEvent(st, plan.evFar, 0));
   launchScatterZ(plan, plan.dZp.get(), z, nrhs, st);
 }
+
+// Right-hand sides in passes of at most maxRhsPerPass columns (the per-node
+// moment rows of M2M / M2T live in shared memory).
+void enqueueMultiply(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
+  const int chunk = maxRhsPerPass(plan);
+  const size_t n = static_cast<size_t>(plan.n);
+  for (int r0 = 0; r0 < nrhs; r0 += chunk)
+    enqueuePass(plan, y + r0 * n, z + r0 * n, std::min(chunk, nrhs - r0), st);
+}
 }  // namespace
 
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t st) {
   ensureWorkspace(plan, nrhs);
   // The legacy default stream cannot be captured: run eagerly there.
+  orderAfterPrevious(plan, st);  // one workspace per plan: calls on different streams run in order
   if (!plan.useGraphs || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
     enqueueMultiply(plan, y, z, nrhs, st);
+    markDone(plan, st);
     return;
   }
   const auto key = std::make_tuple(static_cast<const void*>(y), static_cast<const void*>(z), nrhs, st);
@@ -511,6 +550,7 @@ void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cuda
   }
   it->second.second = ++plan.graphClock;
   FKTB_CUDA(cudaGraphLaunch(it->second.first, st));
+  markDone(plan, st);
 }
 
 }  // namespace fktb

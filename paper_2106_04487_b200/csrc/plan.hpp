@@ -141,6 +141,10 @@ struct DevicePlan {
   // Far-field side stream: S2M -> M2T run concurrently with the near field.
   cudaStream_t side = nullptr;
   cudaEvent_t evGather = nullptr, evFar = nullptr;
+  // Recorded after every multiply / stage on the caller's stream; the next
+  // call (on any stream) waits on it, because the workspaces are per plan.
+  cudaEvent_t evDone = nullptr;
+  bool doneRecorded = false;
   // Monomial-moment S2M (moments.cu) for the compile-time shapes.
   bool useMoments = false;
   int monoCount = 0;
@@ -158,12 +162,6 @@ struct DevicePlan {
   int topPairs = 0;
   DeviceBuffer<int> dTopPairs;
   std::vector<int> farNodesHost; // nodes with a non-empty far set
-  // Symmetric near-field blocks (nearsym.cu).
-  bool nearSym = false;
-  DeviceBuffer<uint32_t> dNearPool;
-  std::vector<FktbBlockTile> blockTilesHost;
-  DeviceBuffer<FktbBlockTile> dBlockTiles;
-  long long symPairs = 0, oneWayPairs = 0;
   // Target shard (shard.cu): owned tree positions [shardLo, shardHi) and the
   // owned sub-range [sub[2b], sub[2b+1]) of every node's far / near list
   // (empty = whole lists).
@@ -202,8 +200,16 @@ std::vector<uint32_t> shardCutsFromLeaves(const std::vector<std::pair<uint32_t, 
                                           uint32_t n);
 unsigned long long farPairWeight(int P);
 void rebuildTiles(DevicePlan& plan);
-// Grow the per-nrhs workspaces (moments, permuted y/z); clears captured graphs.
+// Grow the per-nrhs workspaces (moments, permuted y/z) up to one pass;
+// clears captured graphs.
 void ensureWorkspace(DevicePlan& plan, int nrhs);
+// Right-hand sides one pass of the MVM takes (shared-memory bound; multiply
+// loops over passes).
+constexpr int kMaxRhsPerPass = 64;
+int maxRhsPerPass(const DevicePlan& plan);
+// Stream ordering between calls on one plan (multiply, stage_device).
+void orderAfterPrevious(DevicePlan& plan, cudaStream_t st);
+void markDone(DevicePlan& plan, cudaStream_t st);
 // Number of this library's kernels one multiply launches (memsets excluded).
 long long kernelLaunches(const DevicePlan& plan, int nrhs);
 
@@ -216,8 +222,6 @@ void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, 
 // Near tiles the FP64 near field runs in Gram form (near.cu); the rest run the
 // difference form in a second launch.
 long long nearGramTiles(const DevicePlan& plan);
-void buildNearBlocks(DevicePlan& plan, bool oneWayOnly = false);
-bool launchNearSym(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 // FP32 fast mode when requested and available for (kernel, d), else FP64.
 void launchNearAny(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);

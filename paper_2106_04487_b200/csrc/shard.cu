@@ -134,8 +134,6 @@ void setShard(DevicePlan& plan, int shard, int shards) {
     subranges(t, true, plan.shardLo, plan.shardHi, plan.farSub);
     subranges(t, false, plan.shardLo, plan.shardHi, plan.nearSub);
   }
-  // The symmetric near blocks mix targets of different shards: one-way only.
-  plan.nearSym = false;
   rebuildTiles(plan);
 }
 

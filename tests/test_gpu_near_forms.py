@@ -90,37 +90,3 @@ def test_select_kernels_keep_difference_form(fkt, ref):
     assert g == 0  # explicit r == 0 select
     (g, _), _ = _check(fkt, ref, x, "inverse-r", {}, 4, 0.5, 128, y)
     assert g == 0  # singular kernel
-
-
-def test_mma_near_field_matches_reference(fkt, ref):
-    # the opt-in FP64 tensor-core near field (FKTB_NEAR_MMA=1, read once per
-    # process) in a subprocess: 16 and 8 RHS, Gram, difference and select
-    # forms, every column against the reference's single-RHS multiply
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = r"""
-import sys, numpy as np
-sys.path.insert(0, %r)
-import paper_2106_04487_b200 as fkt
-from oracle import ref
-rng = np.random.default_rng(11)
-x = rng.random((6000, 2))
-for nr in (16, 8):
-    Y = rng.standard_normal((6000, nr))
-    for name, prm, diag in (("cauchy", {"sigma": 0.5}, None), ("inverse-r", {}, None),
-                            ("matern32", {"sigma": 1.0, "rho": 0.2}, 0.3)):
-        kw = {} if diag is None else {"diagonal": diag}
-        pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(name, prm),
-                      fkt.FktOptions(p=4, theta=0.6, leafCapacity=128, **kw))
-        rp = ref.RefPlan(x, name, prm, p=4, theta=0.6, leaf=128, diagonal=diag)
-        Z = pl.multiply(Y)
-        for c in range(nr):
-            err = fkt.relativeError(Z[:, c], rp.multiply(Y[:, c].copy()))
-            assert err <= 1e-10, (name, nr, c, err)
-print("ok")
-""" % root
-    env = dict(os.environ, FKTB_NEAR_MMA="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900, cwd=root)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
