@@ -348,7 +348,7 @@ def run_ours(args):
                             else "single GPU"),
             "l2": "inputs larger than L2: far lists %.0f MB + near lists %.0f MB + coordinates %.0f MB per step"
                   % (info["far_total"] * 4 / 1e6, info["near_total"] * 4 / 1e6, n * c["d"] * 8 / 1e6),
-            "plan_seconds": plan_s,
+            "plan_seconds": plan_s, "plan_phases": pl.plan_phases(),
             "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
             "near_evals": nev_all, "coefficients": P,
         },

@@ -240,6 +240,11 @@ int fkt_compression_ranks(const char* kernel, const char* const* keys, const dou
 double fkt_addition_normalizer(int d, int k);
 long long fkt_harmonic_count(int d, int k);
 
+/* Plan-time phases in seconds, in this order: tree (K1), interaction sets
+ * (K2), exact tables, work tiles, near-field geometry rows, moment plan,
+ * other (workspaces, drains). Writes min(count, 7) values. */
+int fkt_plan_phases(fkt_plan_t plan, double* seconds, int count);
+
 /* Measurement support: FMA-pipe peak (FLOP/s, FMA = 2) of the current device,
  * fp64 (fp32 = 0) or fp32 (fp32 = 1): the roofline denominator for the
  * FP64-bound kernels. */

@@ -412,6 +412,14 @@ class FktPlan:
     def info(self) -> dict:
         return {f: getattr(self._info, f) for f, _ in _L.FktPlanInfoC._fields_}
 
+    PLAN_PHASES = ("tree", "sets", "tables", "tiles", "near_rows", "moments", "other")
+
+    def plan_phases(self) -> dict:
+        """Plan-time seconds per phase (fkt_plan_phases)."""
+        out = (C.c_double * len(self.PLAN_PHASES))()
+        _check(lib.fkt_plan_phases(self._h, out, len(self.PLAN_PHASES)))
+        return dict(zip(self.PLAN_PHASES, list(out)))
+
     def tree(self) -> PartitionTree:
         if self._tree is None:
             th = lib.fkt_plan_tree(self._h)

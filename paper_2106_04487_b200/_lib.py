@@ -140,6 +140,7 @@ SIGNATURES = {
     "fkt_harmonic_count": (C.c_longlong, C.c_int, C.c_int),
     "fkt_fma_peak": (C.c_int, C.c_int, _d),
     "fkt_fp64_peaks": (C.c_int, _d, _d),
+    "fkt_plan_phases": (C.c_int, C.c_void_p, _d, C.c_int),
     "fkt_synth_cloud": (C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_uint64, _d, _d),
     "fkt_synth_config": (C.c_int, C.c_int, C.c_int, C.c_uint64, _d, _d),
     "fkt_config_dims": (C.c_int, C.c_int, _i32, _i32),

@@ -363,6 +363,12 @@ int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info) {
   });
 }
 
+int fkt_plan_phases(fkt_plan_t plan, double* seconds, int count) {
+  return guarded([&] {
+    for (int i = 0; i < count && i < fktb::kPhaseCount; ++i) seconds[i] = plan->plan->phaseSeconds[i];
+  });
+}
+
 int fkt_plan_multiply(fkt_plan_t plan, const double* y, double* z, int nrhs) {
   return guarded([&] {
     if (nrhs < 1) throw DimensionMismatch("multiply: nrhs must be >= 1");

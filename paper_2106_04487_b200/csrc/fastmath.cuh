@@ -57,6 +57,19 @@ __device__ __forceinline__ double rsqrt_nr_half(double x) {
   return fma(y0, e, y0);
 }
 
+// sqrt(x / 2) for x > 0: callers pass TWICE the squared distance (Gram rows
+// scaled by 2), so the Newton step's factor 1/2 rides on the argument and the
+// step costs 3 FP64 ops (DMUL + 2 DFMA) instead of 4. The seed is MUFU rsqrt
+// of 2x (exponent + 1 on the high word, integer pipe): y0 ~ 1/sqrt(2x),
+// h = x y0 ~ sqrt(x/2), e = 1/2 - h y0 = -(delta + delta^2/2) for the seed
+// error delta, and h (1 + e) has error O(delta^2).
+__device__ __forceinline__ double sqrt_nr_half(double x) {
+  const double y0 = rsqrt_approx(__hiloint2double(__double2hiint(x) + 0x00100000, 0));
+  const double h = x * y0;
+  const double e = fma(-h, y0, 0.5);
+  return fma(h, e, h);
+}
+
 // sqrt(x) for x > 0 (callers bias squared distances by kQBias so x == 0
 // never reaches the approximation's infinity).
 __device__ __forceinline__ double sqrt_nr(double x) {
@@ -155,6 +168,7 @@ __device__ __forceinline__ double exp_table_at(const double* __restrict__ tab, i
   return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + off);
 }
 
+// tab: the PRE-COMPENSATED table (see the exponent step below).
 template <int REP = 1, int BITS = 9, bool CLAMP_LO = true, bool CLAMP_HI = true>
 __device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict__ tab, int colBytes) {
   static_assert(BITS >= 6, "degree-4 polynomial needs |f| <= ln2/2^7");
@@ -179,11 +193,12 @@ __device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict_
   p = fma(f, p, 1.0);
   p = fma(f, p, 1.0);
   const double tj = exp_table_at<REP, BITS>(tab, kb, colBytes);
-  // exponent: hi(tj) + ((kb >> BITS) << 20); the shift is opaque to the
-  // front end so ptxas forms SHF + LEA (it would otherwise emit shl, and, add)
-  int e;
-  asm("shr.s32 %0, %1, %2;" : "=r"(e) : "r"(kb), "n"(BITS));
-  const unsigned eh = static_cast<unsigned>(__double2hiint(tj)) + (static_cast<unsigned>(e) << 20);
+  // exponent: the table is stored pre-compensated (expTableDevice(bits,
+  // true): entry j's high word minus j << (20 - BITS)), so one shift-add,
+  // hi(tj) + (kb << (20 - BITS)), adds floor(k / 2^BITS) << 20 to the true
+  // entry's exponent: kb << (20 - BITS) = (e << 20) + (j << (20 - BITS)) mod
+  // 2^32 for k = e 2^BITS + j (the 0x4b400000 of kb shifts out)
+  const unsigned eh = static_cast<unsigned>(__double2hiint(tj)) + (static_cast<unsigned>(kb) << (20 - BITS));
   return __hiloint2double(static_cast<int>(eh), __double2loint(tj)) * p;
 }
 

@@ -40,34 +40,37 @@ struct FastKernel {
   // Matern-3/2 takes sqrt(q): its Gram q gets an additive bias (near.cu).
   static constexpr bool gramBiased = KID == FKTB_KERNEL_MATERN32;
 
-  template <bool FI, int REP, bool CLAMP_LO = true, bool CLAMP_HI = true>
+  // Matern-3/2's Gram rows carry TWICE the squared distance (sqrt_nr_half).
+  static constexpr double gramScale = KID == FKTB_KERNEL_MATERN32 ? 2.0 : 1.0;
+
+  template <int REP, bool CLAMP_LO = true, bool CLAMP_HI = true>
   __device__ static __forceinline__ double expn(double u, const double* tab, int colBytes) {
-    if constexpr (FI) return exp_neg_fi<REP, kNearExpBits, CLAMP_LO, CLAMP_HI>(u, tab, colBytes);
-    else return exp_neg<REP, kNearExpBits>(u, tab + colBytes / 8);
+    return exp_neg_fi<REP, kNearExpBits, CLAMP_LO, CLAMP_HI>(u, tab, colBytes);
   }
 
   // canonical K at scaled squared distance q (> 0 unless the select handles
-  // 0); GRAM: q already carries gramOffset. FI: FP32-indexed exp. tab: the
-  // REP-replicated exp table, colBytes: 8 * this lane's column.
-  template <int REP, bool FI = false, bool GRAM = false>
+  // 0); GRAM: q already carries gramOffset and gramScale. tab: the
+  // REP-replicated, pre-compensated exp table (exp_neg_fi), colBytes: 8 *
+  // this lane's column.
+  template <int REP, bool GRAM = false>
   __device__ static __forceinline__ double eval(double q, const double* tab, int colBytes = 0) {
     // Gram q may round slightly below 0: Matern's sources carry a bias that
     // covers the rounding (near.cu gramBias; sqrt(q) >= 2^-127 as the
     // FP32-indexed exp needs), the other Gram kernels take 1 + q. The Gram
     // bound keeps sqrt(q) and 1 + q far below the exp clamp: no clamps here.
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
-      double u = sqrt_nr(q);
-      if constexpr (FI && !GRAM) u = clamp_exp_arg(u);  // in place: the (1 + u) factor uses the same u
-      const double e = expn<FI, REP, !GRAM, false>(u, tab, colBytes);
+      double u = GRAM ? sqrt_nr_half(q) : sqrt_nr(q);  // Gram q = 2 r^2
+      if constexpr (!GRAM) u = clamp_exp_arg(u);  // in place: the (1 + u) factor uses the same u
+      const double e = expn<REP, !GRAM, false>(u, tab, colBytes);
       return fma(u, e, e);
     } else if constexpr (KID == FKTB_KERNEL_MATERN12 || KID == FKTB_KERNEL_EXPONENTIAL) {
-      return expn<FI, REP, !GRAM, true>(sqrt_nr(q), tab, colBytes);
+      return expn<REP, !GRAM, true>(sqrt_nr(q), tab, colBytes);
     } else if constexpr (KID == FKTB_KERNEL_CAUCHY) {
       return rcp_nr(GRAM ? q : 1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_RATIONAL_QUADRATIC) {
       return rsqrt_nr(GRAM ? q : 1.0 + q);
     } else if constexpr (KID == FKTB_KERNEL_GAUSSIAN) {
-      return expn<FI, REP, !GRAM, !GRAM>(q, tab, colBytes);
+      return expn<REP, !GRAM, !GRAM>(q, tab, colBytes);
     } else if constexpr (KID == FKTB_KERNEL_INVERSE_R) {
       return rsqrt_nr_half(q);  // q = r^2 / 2: fastScales scales by 1/sqrt(2)
     } else {

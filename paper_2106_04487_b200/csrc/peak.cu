@@ -5,8 +5,11 @@
 // tensor core share it on B200, profiles/r01_probes.txt):
 //   * DFMA: 148 SMs x 8 CTAs x 256 threads, 8 independent chains per thread;
 //   * DMMA: mma.sync m8n8k4 f64, 8 independent accumulators per warp.
-// Each probe first runs a long warm-up launch (clocks up), then three run
-// lengths x three repetitions; the best time counts. FP32: the FFMA chains.
+// Each probe first runs a warm-up launch (clocks up), then short bursts (~1-2
+// ms: the kernel timed alone, before the board power limit pulls the clock
+// down -- a 17 ms DFMA run measured 34.2 TF, the 1-2 ms bursts 36.8-37.0 on
+// the same B200), two lengths x five repetitions; the best counts. FP32: the
+// FFMA chains.
 // Returns FLOP/s (FMA = 2 flops).
 #include <cuda_runtime.h>
 
@@ -17,21 +20,27 @@
 
 namespace {
 
+// x <- x * s + b with the multiplier s warp-uniform (a uniform-register
+// operand) and b per thread: two register-pair operands per DFMA. With both
+// s and b in vector registers (three register pairs per DFMA) the same loop
+// measured 34.1 TF against 36.9 -- register-file operand bandwidth, not the
+// FP64 pipe, then bounds it.
 template <class T>
-__global__ void fma_chain(T* out, int iters, T a, T b) {
+__global__ void fma_chain(T* out, int iters, T s) {
   T x[8];
+  const T b = threadIdx.x * T(1e-3);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * T(1e-3) + T(c) * T(0.5);
+  for (int c = 0; c < 8; ++c) x[c] = T(c) * T(0.5);
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 16; ++u)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) x[c] = fma(x[c], a, b);
+      for (int c = 0; c < 8; ++c) x[c] = fma(x[c], s, b);
   }
-  T s = 0;
+  T sum = 0;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) s += x[c];
-  if (s == T(-12345.678)) out[0] = s;  // keep the chains alive
+  for (int c = 0; c < 8; ++c) sum += x[c];
+  if (sum == T(-12345.678)) out[0] = sum;  // keep the chains alive
 }
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
@@ -40,16 +49,14 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void dmma_chain(double* out, int iters, double a, double b) {
+__global__ void dmma_chain(double* out, int iters, double b) {
   double c[8][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = i;
-  const double x = a + threadIdx.x * 1e-9;
+  const double x = threadIdx.x * 1e-3;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dmma884(c[i], x, b);
+    for (int i = 0; i < 8; ++i) dmma884(c[i], x, b);
   }
   double s = 0;
 #pragma unroll
@@ -63,11 +70,11 @@ double bestRate(L launch, double flopsPerIter, int baseIters) {
   cudaEvent_t e0, e1;
   FKTB_CUDA(cudaEventCreate(&e0));
   FKTB_CUDA(cudaEventCreate(&e1));
-  launch(baseIters * 4);  // warm-up: bring the clocks up
+  launch(baseIters);  // warm-up: bring the clocks up
   double best = 0.0;
-  for (int len : {1, 2, 4}) {
+  for (int len : {1, 2}) {
     const int iters = baseIters * len;
-    for (int rep = 0; rep < 3; ++rep) {
+    for (int rep = 0; rep < 5; ++rep) {
       FKTB_CUDA(cudaEventRecord(e0));
       launch(iters);
       FKTB_CUDA(cudaEventRecord(e1));
@@ -96,8 +103,8 @@ double measureFma() {
   T* out = nullptr;
   FKTB_CUDA(cudaMalloc(&out, sizeof(T)));
   const double perIter = 2.0 * 8 * 16 * static_cast<double>(blocks) * threads;
-  const double r = bestRate([&](int it) { fma_chain<T><<<blocks, threads>>>(out, it, T(0.999999), T(1e-7)); },
-                            perIter, sizeof(T) == 8 ? 1000 : 2000);
+  const double r = bestRate([&](int it) { fma_chain<T><<<blocks, threads>>>(out, it, T(1.0000001)); }, perIter,
+                            sizeof(T) == 8 ? 250 : 500);
   cudaFree(out);
   return r;
 }
@@ -107,8 +114,8 @@ double measureDmma() {
   double* out = nullptr;
   FKTB_CUDA(cudaMalloc(&out, sizeof(double)));
   const double warps = blocks * threads / 32.0;
-  const double perIter = warps * 4 * 8 * (2.0 * 8 * 8 * 4);
-  const double r = bestRate([&](int it) { dmma_chain<<<blocks, threads>>>(out, it, 1.0000001, 1e-7); }, perIter, 500);
+  const double perIter = warps * 8 * (2.0 * 8 * 8 * 4);
+  const double r = bestRate([&](int it) { dmma_chain<<<blocks, threads>>>(out, it, 1.0000001); }, perIter, 500);
   cudaFree(out);
   return r;
 }

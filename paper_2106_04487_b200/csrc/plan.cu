@@ -185,6 +185,11 @@ void buildTiles(DevicePlan& plan) {
     const long long n1 = plan.nearSub.empty() ? t.nearOff[B + 1] : plan.nearSub[2 * B + 1];
     for (long long s = n0; s < n1; s += nt) plan.nearTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(nt, n1 - s)), s});
   }
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    buildNearRows(plan);  // streaming near field: Gram-first tile order (+ rows, once)
+    plan.phaseSeconds[kPhaseNearRows] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
   auto upload = [&](DeviceBuffer<FktbTile>& dst, const std::vector<FktbTile>& src) {
     dst.resize(std::max<size_t>(1, src.size()));
     if (!src.empty())
@@ -341,6 +346,14 @@ void ensureWorkspace(DevicePlan& plan, int nrhs) {
   const size_t n = static_cast<size_t>(plan.n);
   plan.dYp.resize(n * nrhs);
   plan.dZp.resize(n * nrhs);
+  if (plan.nearRowsBuilt) {
+    // per-pass source-major weights of R <= min(nrhs, 16) columns (a power
+    // of two; one column rides in the source rows)
+    int r = 1;
+    while (r * 2 <= std::min(nrhs, 16)) r *= 2;
+    if (r > 1) plan.dNearW.resize(n * r);
+    if (plan.dNearCounter.size() == 0) plan.dNearCounter.resize(2);
+  }
   plan.dMoments.resize(std::max<size_t>(1, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs));
   plan.nrhsCap = nrhs;
 }
@@ -390,9 +403,19 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   FKTB_CUDA(cudaEventCreateWithFlags(&plan->evGather, cudaEventDisableTiming));
   FKTB_CUDA(cudaEventCreateWithFlags(&plan->evFar, cudaEventDisableTiming));
   FKTB_CUDA(cudaEventCreateWithFlags(&plan->evDone, cudaEventDisableTiming));
+  // phase timings (fkt_plan_phases): each phase ends with its stream drained
+  auto tPrev = std::chrono::steady_clock::now();
+  auto phase = [&](int i) {
+    FKTB_CUDA(cudaStreamSynchronize(plan->stream));
+    const auto now = std::chrono::steady_clock::now();
+    plan->phaseSeconds[i] += std::chrono::duration<double>(now - tPrev).count();
+    tPrev = now;
+  };
   plan->tree = std::make_unique<DeviceTree>();
   buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
+  phase(kPhaseTree);
   computeSetsGpu(*plan->tree, options.theta);
+  phase(kPhaseSets);
 
   plan->compressed = compress;
   if (bh) {
@@ -408,20 +431,24 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     if (compress) plan->factors = radialCompression(kernel, *table, plan->options.p);
     buildFarParams(*plan);
   }
+  phase(kPhaseTables);
   buildTiles(*plan);
+  phase(kPhaseTiles);
+  plan->phaseSeconds[kPhaseTiles] -= plan->phaseSeconds[kPhaseNearRows];  // buildTiles timed the rows itself
   if (bh) {
     buildBarnesHut(*plan);
   } else {
     const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
   }
+  phase(kPhaseMoments);
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
   (void)expTableDevice();  // lazy device tables: initialise outside any graph capture
-  (void)expTableDevice(kNearExpBits);
+  (void)expTableDevice(kNearExpBits, true);
   if (const char* g = std::getenv("FKTB_GRAPHS")) plan->useGraphs = std::atoi(g) != 0;
-  FKTB_CUDA(cudaStreamSynchronize(plan->stream));
+  phase(kPhaseOther);
   plan->planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return plan;
 }
@@ -459,9 +486,9 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
     k += plan.options.barnesHut ? 1 : chunks(plan.P);
   }
   if (!plan.nearTilesHost.empty()) {
-    // FP64 near field: one launch per pair form present (near.cu)
-    const long long g = plan.options.nearPrecision == 32 ? 0 : nearGramTiles(plan);
-    k += (g > 0) + (g < static_cast<long long>(plan.nearTilesHost.size()));
+    // FP32 mode: one launch (near32.cu); FP64: per RHS pass, one launch per
+    // pair form present (+ the weight kernel when the pass needs it, near.cu)
+    k += plan.options.nearPrecision == 32 ? 1 : nearLaunches(plan, nrhs);
   }
   k += !plan.farTilesHost.empty();
   return k;

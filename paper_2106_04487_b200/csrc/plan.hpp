@@ -136,6 +136,9 @@ struct DevicePlan {
   DeviceBuffer<double> dYio, dZio;       // staging for host-buffer multiplies
   int nrhsCap = 0;
   double planSeconds = 0.0;
+  // plan-time phases (seconds): tree, sets, exact tables, tiles, near rows,
+  // moment plan, other (fkt_plan_phases)
+  double phaseSeconds[7] = {};
   std::mutex mutex;                       // multiply() is serialised per plan
   cudaStream_t stream = nullptr;
   // Far-field side stream: S2M -> M2T run concurrently with the near field.
@@ -162,6 +165,14 @@ struct DevicePlan {
   int topPairs = 0;
   DeviceBuffer<int> dTopPairs;
   std::vector<int> farNodesHost; // nodes with a non-empty far set
+  // Streaming near field (near.cu near_stream): geometry rows (n x GS, plan
+  // time), the factored Gaussian's per-source weight factor, the per-pass
+  // source-major weights, two tile-claim counters; near tiles are ordered
+  // Gram form first (nearGramTileCount of them).
+  bool nearRowsBuilt = false;
+  long long nearGramTileCount = 0;
+  DeviceBuffer<double> dNearRows, dNearFac, dNearW;
+  DeviceBuffer<int> dNearCounter;
   // Target shard (shard.cu): owned tree positions [shardLo, shardHi) and the
   // owned sub-range [sub[2b], sub[2b+1]) of every node's far / near list
   // (empty = whole lists).
@@ -182,6 +193,8 @@ struct DevicePlan {
   bool useGraphs = true;
 };
 
+enum { kPhaseTree = 0, kPhaseSets, kPhaseTables, kPhaseTiles, kPhaseNearRows, kPhaseMoments, kPhaseOther, kPhaseCount };
+
 std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
                                        const PlanOptions& options);
 void destroyPlan(DevicePlan* plan);
@@ -190,7 +203,7 @@ void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cuda
 
 // 2^(j/2^bits), j < 2^bits, in device memory (default 64 entries: the far
 // kernels; the near field uses kNearExpBits).
-const double* expTableDevice(int bits = 6);
+const double* expTableDevice(int bits = 6, bool compensated = false);
 
 // Kernel launchers (near.cu, far.cu, dense.cu).
 // Multi-GPU target sharding (shard.cu).
@@ -219,6 +232,10 @@ void launchBHSums(const DevicePlan& plan, const double* yp, double* totals, int 
 void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int nrhs, cudaStream_t stream);
 
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
+// Streaming near field: plan-time rows and tile order (near.cu); launches
+// per multiply.
+void buildNearRows(DevicePlan& plan);
+long long nearLaunches(const DevicePlan& plan, int nrhs);
 // Near tiles the FP64 near field runs in Gram form (near.cu); the rest run the
 // difference form in a second launch.
 long long nearGramTiles(const DevicePlan& plan);

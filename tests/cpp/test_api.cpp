@@ -50,9 +50,12 @@ static void dense_basics() {  // test_transform.cpp:12-27
   CHECK(std::abs(z[0] - 1.0) < 1e-15);
   CHECK(std::abs(z[1] - std::exp(-1.0)) < 1e-14);
   CHECK_THROWS_AS(denseMultiply(pair, *k, y1), DimensionMismatchError);
-  // singular kernel, no diagonal convention: the reference's own exception
-  // type (kernels.hpp:22-26), which gp.cpp:13 catches by type
-  CHECK_THROWS_AS(denseMultiply(pair, *makeKernel("inverse-r"), y), SingularAtZeroError);
+  // no diagonal convention (every built-in registers one, kernels.cpp:37-160):
+  // the reference's own exception type (kernels.hpp:22-26), which gp.cpp:13
+  // catches by type
+  IsotropicKernel custom("custom", {}, [](double r) { return 1.0 / r; }, std::nullopt);
+  CHECK_THROWS_AS(custom(0.0), SingularAtZeroError);
+  CHECK(std::abs(custom(0.0, 2.5) - 2.5) < 1e-15);
 }
 
 static void single_leaf_exact() {  // test_transform.cpp:38-50
