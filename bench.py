@@ -210,7 +210,8 @@ def run_ours(args):
     x, w = fkt.synthConfig(args.cfg, n)
     t0 = time.perf_counter()
     pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(c["kernel"], c["params"]),
-                  fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"], nearPrecision=args.near_precision))
+                  fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"], nearPrecision=args.near_precision,
+                                 deterministic=args.deterministic))
     plan_s = time.perf_counter() - t0
     info = pl.info()
     wcols = w.reshape(n, nrhs) if nrhs > 1 else w
@@ -349,6 +350,7 @@ def run_ours(args):
             "l2": "inputs larger than L2: far lists %.0f MB + near lists %.0f MB + coordinates %.0f MB per step"
                   % (info["far_total"] * 4 / 1e6, info["near_total"] * 4 / 1e6, n * c["d"] * 8 / 1e6),
             "plan_seconds": plan_s, "plan_phases": pl.plan_phases(),
+            "deterministic": bool(args.deterministic),
             "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
             "near_evals": nev_all, "coefficients": P,
         },
@@ -491,6 +493,8 @@ def main():
                     help="use the target-sharded multi-GPU path even at one rank (it is automatic for N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=3, help="timed reference MVMs for cpu_baseline (median)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise reproducible MVM (FktOptions.deterministic: fixed-order sums, no atomics)")
     ap.add_argument("--near-precision", type=int, default=64, choices=[64, 32],
                     help="32 = FP32 fast near-field mode (not the headline; parity gate is FP64)")
     args = ap.parse_args()

@@ -51,6 +51,7 @@ struct FktOptions {
   int threads = 0;             // CPU knob of the reference, ignored
   std::optional<double> diagonal;
   int nearPrecision = 64;      // additive: 32 selects the FP32 fast near field
+  bool deterministic = false;  // additive: bitwise reproducible z (no atomics into z / moments)
 };
 
 class FktPlan {

@@ -48,6 +48,9 @@ typedef struct fkt_options {
   int has_diagonal;
   double diagonal;
   int near_precision;  /* additive extension: 64 (default, FP64) or 32 (FP32 fast near field) */
+  int deterministic;   /* additive extension: 1 = bitwise reproducible z (fixed-order sums, no
+                          atomics into z or the moments); the reference merges
+                          its per-thread buffers in a fixed order (transform.cpp:194-203) */
 } fkt_options;
 
 typedef struct fkt_plan_s* fkt_plan_t;

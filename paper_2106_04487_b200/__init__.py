@@ -197,11 +197,13 @@ class FktOptions:
     threads: int = 0
     diagonal: Optional[float] = None
     nearPrecision: int = 64  # additive: 32 selects the FP32 fast near field
+    deterministic: bool = False  # additive: bitwise reproducible z (fixed-order sums)
 
     def _c(self) -> _L.FktOptionsC:
         return _L.FktOptionsC(int(self.p), float(self.theta), int(self.leafCapacity), int(self.compression),
                               int(bool(self.eagerOperators)), int(bool(self.barnesHut)), int(self.threads),
-                              int(self.diagonal is not None), float(self.diagonal or 0.0), int(self.nearPrecision))
+                              int(self.diagonal is not None), float(self.diagonal or 0.0), int(self.nearPrecision),
+                              int(bool(self.deterministic)))
 
 
 # --- tree view -----------------------------------------------------------------

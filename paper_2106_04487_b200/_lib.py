@@ -40,6 +40,7 @@ class FktOptionsC(C.Structure):
         ("has_diagonal", C.c_int),
         ("diagonal", C.c_double),
         ("near_precision", C.c_int),
+        ("deterministic", C.c_int),
     ]
 
 

@@ -245,6 +245,7 @@ fkt_options toC(const FktOptions& f) {
   o.has_diagonal = f.diagonal ? 1 : 0;
   o.diagonal = f.diagonal.value_or(0.0);
   o.near_precision = f.nearPrecision;
+  o.deterministic = f.deterministic ? 1 : 0;
   return o;
 }
 }  // namespace

@@ -43,8 +43,10 @@ __global__ void bh_com_kernel(int n, int d, const double* pc, const uint32_t* be
   }
 }
 
-// totals[r][node] += sum of yp over one source tile of the node.
-__global__ void bh_sum_kernel(int n, int nodes, int nrhs, const FktbTile* tiles, const double* yp, double* totals) {
+// totals[r][node] += sum of yp over one source tile of the node (deterministic
+// mode: part[tile][r] = the tile's sum, reduced in tile order by det.cu).
+__global__ void bh_sum_kernel(int n, int nodes, int nrhs, const FktbTile* tiles, const double* yp, double* totals,
+                              double* part) {
   const FktbTile tile = tiles[blockIdx.x];
   __shared__ double red[kThreads / 32];
   for (int r = 0; r < nrhs; ++r) {
@@ -56,7 +58,10 @@ __global__ void bh_sum_kernel(int n, int nodes, int nrhs, const FktbTile* tiles,
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < kThreads / 32; ++w) t += red[w];
-      atomicAdd(totals + static_cast<size_t>(r) * nodes + tile.node, t);
+      if (part)
+        part[static_cast<size_t>(blockIdx.x) * nrhs + r] = t;
+      else
+        atomicAdd(totals + static_cast<size_t>(r) * nodes + tile.node, t);
     }
     __syncthreads();
   }
@@ -65,7 +70,7 @@ __global__ void bh_sum_kernel(int n, int nodes, int nrhs, const FktbTile* tiles,
 // z[t] += K(|x_t - com_b|) * totals[r][b] for the far-list entries of one tile.
 __global__ void bh_far_kernel(int n, int d, int nodes, int nrhs, const double* pc, const double* com,
                               const FktbTile* tiles, const uint32_t* farPos, const FktbKernelDesc kd,
-                              const double* totals, double* zp) {
+                              const double* totals, const ZOut out) {
   const FktbTile tile = tiles[blockIdx.x];
   for (int i = threadIdx.x; i < tile.count; i += kThreads) {
     const uint32_t pos = farPos[tile.start + i];
@@ -75,8 +80,7 @@ __global__ void bh_far_kernel(int n, int d, int nodes, int nrhs, const double* p
       dist2 = fma(t, t, dist2);
     }
     const double k = kernel_value_rt(kd, sqrt(dist2));
-    for (int r = 0; r < nrhs; ++r)
-      atomicAdd(zp + static_cast<size_t>(r) * n + pos, k * totals[static_cast<size_t>(r) * nodes + tile.node]);
+    for (int r = 0; r < nrhs; ++r) out.add(r, tile.start + i, pos, k * totals[static_cast<size_t>(r) * nodes + tile.node]);
   }
 }
 
@@ -93,8 +97,10 @@ void buildBarnesHut(DevicePlan& plan) {
 void launchBHSums(const DevicePlan& plan, const double* yp, double* totals, int nrhs, cudaStream_t st) {
   const int tiles = static_cast<int>(plan.s2mTilesHost.size());
   if (tiles == 0) return;
-  bh_sum_kernel<<<tiles, kThreads, 0, st>>>(plan.n, plan.tree->nodes, nrhs, plan.dS2mTiles.get(), yp, totals);
+  double* part = plan.options.deterministic ? plan.dTilePart.get() : nullptr;
+  bh_sum_kernel<<<tiles, kThreads, 0, st>>>(plan.n, plan.tree->nodes, nrhs, plan.dS2mTiles.get(), yp, totals, part);
   FKTB_CUDA(cudaGetLastError());
+  if (part) launchDetTileSum(plan, part, 1, nrhs, totals, st);
 }
 
 void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int nrhs, cudaStream_t st) {
@@ -104,7 +110,7 @@ void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int n
   FktbKernelDesc kd;
   fillKernelDesc(plan.kernel, kd);
   bh_far_kernel<<<tiles, kThreads, 0, st>>>(t.n, t.d, t.nodes, nrhs, t.pc.get(), plan.dCom.get(), plan.dFarTiles.get(),
-                                            t.dFarPos.get(), kd, totals, zp);
+                                            t.dFarPos.get(), kd, totals, zoutFor(plan, zp, nrhs, true));
   FKTB_CUDA(cudaGetLastError());
 }
 

@@ -164,6 +164,7 @@ void fkt_default_options(fkt_options* o) {
   o->has_diagonal = 0;
   o->diagonal = 0.0;
   o->near_precision = 64;
+  o->deterministic = 0;
 }
 
 }  // extern "C"
@@ -186,6 +187,7 @@ fktb::PlanOptions toPlanOptions(const fkt_options* opt) {
   if (o.near_precision != 64 && o.near_precision != 32)
     throw std::invalid_argument("near_precision must be 64 or 32");
   po.nearPrecision = o.near_precision;
+  po.deterministic = o.deterministic != 0;
   if (!po.barnesHut && po.p > fktb::kMaxExpansionOrder)
     throw OrderTooLarge("expansion order " + std::to_string(po.p) + " exceeds the supported cap " +
                         std::to_string(fktb::kMaxExpansionOrder));
@@ -251,7 +253,8 @@ unsigned long long g_cacheClock = 0;
 bool sameOptions(const fkt_options& a, const fkt_options& b) {
   return a.p == b.p && a.theta == b.theta && a.leaf_capacity == b.leaf_capacity && a.compression == b.compression &&
          a.barnes_hut == b.barnes_hut && a.has_diagonal == b.has_diagonal &&
-         (!a.has_diagonal || a.diagonal == b.diagonal) && a.near_precision == b.near_precision;
+         (!a.has_diagonal || a.diagonal == b.diagonal) && a.near_precision == b.near_precision &&
+         (a.deterministic != 0) == (b.deterministic != 0);
 }
 
 void evictLocked() {
@@ -415,8 +418,14 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
         break;
       case 1: fktb::launchS2MAny(p, p.dYp.get(), p.dMoments.get(), nrhs, st); break;
       case 2: fktb::launchNearAny(p, p.dYp.get(), p.dZp.get(), nrhs, st); break;
-      case 3: fktb::launchM2T(p, p.dMoments.get(), p.dZp.get(), nrhs, st); break;
-      case 4: fktb::launchScatterZ(p, p.dZp.get(), z_dev, nrhs, st); break;
+      case 3:
+        fktb::launchM2T(p, p.dMoments.get(), p.dZp.get(), nrhs, st);
+        if (p.options.deterministic) fktb::launchDetReduce(p, nullptr, nrhs, true, st);
+        break;
+      case 4:
+        if (p.options.deterministic) fktb::launchDetReduce(p, p.dZp.get(), nrhs, false, st);
+        fktb::launchScatterZ(p, p.dZp.get(), z_dev, nrhs, st);
+        break;
       default: throw std::invalid_argument("stage must be 0..4");
     }
     fktb::markDone(p, st);

@@ -81,6 +81,25 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* scratc
   return r;
 }
 
+// Where the near / far kernels put the result of one (target, list entry): default, an FP64 atomic into z (tree order, n per right-hand side);
+// deterministic plans (FktOptions::deterministic, det.cu), a plain store of
+// the partial at its list entry, right-hand sides minor (coalesced: a tile's
+// entries are consecutive), which a fixed-order per-target sum turns into z
+// (bitwise reproducible).
+struct ZOut {
+  double* zp;        // n per RHS
+  double* part;      // deterministic: partials [entry][rhs] (nullptr: atomics)
+  long long stride;  // right-hand sides per entry (the pass)
+  long long base;    // first entry of this list (near entries, then far entries)
+  int n;
+  __device__ __forceinline__ void add(int rhs, long long entry, int pos, double v) const {
+    if (part)
+      part[static_cast<size_t>(base + entry) * stride + rhs] = v;
+    else
+      atomicAdd(zp + static_cast<size_t>(rhs) * n + pos, v);
+  }
+};
+
 }  // namespace fktb
 
 #endif

@@ -33,7 +33,7 @@ struct NearArgs {
   const FktbTile* tiles;
   const uint32_t* nearPos;
   const double* yp;  // permuted weights, n x nrhs
-  double* zp;        // permuted output, n x nrhs
+  ZOut out;          // permuted output, n x nrhs (atomics or deterministic slots)
   FktbKernelDesc kd;
 };
 
@@ -95,10 +95,9 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constan
         }
       }
     }
-    double* z = A.zp + static_cast<size_t>(rhs) * n;
 #pragma unroll
     for (int i = 0; i < kNearTPT; ++i) {
-      if (tpos[i] >= 0) atomicAdd(z + tpos[i], acc[i]);
+      if (tpos[i] >= 0) A.out.add(rhs, tile.start + threadIdx.x + i * kNearThreads, tpos[i], acc[i]);
       acc[i] = 0.0;
     }
   }
@@ -264,7 +263,7 @@ struct StreamArgs {
   const uint32_t* nearPos;
   const double* rows;  // source rows, n x GS (single-RHS weight in the last slot)
   const double* w;     // R > 1: source-major weights, n x RP
-  double* zp;          // permuted output, n per RHS (this pass's first column)
+  ZOut out;            // permuted output, n per RHS (this pass's first column)
   const double* center;
   const double* limit2;
   double sc;         // coordinate scale
@@ -524,7 +523,7 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
         if (tpos[i] >= 0) {
           const double f = FAC ? A.scale * exp(-tn[i]) : A.scale;  // factored Gaussian: e^-|t|^2
 #pragma unroll
-          for (int r = 0; r < R; ++r) atomicAdd(A.zp + static_cast<size_t>(r) * n + tpos[i], acc[i][r] * f);
+          for (int r = 0; r < R; ++r) A.out.add(r, tile.start + base + lane + i * 32, tpos[i], acc[i][r] * f);
         }
     }
     t = tn1;
@@ -560,7 +559,7 @@ NearFast nearFastConfig(const DevicePlan& plan) {
 }
 
 template <int KID, int D, bool SEL, int TPT, int R, bool GRAM>
-void launchStream(const DevicePlan& plan, const NearFast& f, const double* w, double* zp, int tile0, int tile1,
+void launchStream(const DevicePlan& plan, const NearFast& f, const double* w, const ZOut& out, int tile0, int tile1,
                   int* counter, cudaStream_t st) {
   if (tile1 <= tile0) return;
   using FK = FastKernel<KID>;
@@ -589,7 +588,7 @@ void launchStream(const DevicePlan& plan, const NearFast& f, const double* w, do
   A.nearPos = t.dNearPos.get();
   A.rows = plan.dNearRows.get();
   A.w = w;
-  A.zp = zp;
+  A.out = out;
   A.center = t.dCenter.get();
   A.limit2 = t.dLimit2.get();
   A.sc = f.sc;
@@ -604,16 +603,16 @@ void launchStream(const DevicePlan& plan, const NearFast& f, const double* w, do
 
 // One RHS pass of R columns: both pair forms (Gram tiles first).
 template <int KID, int D, bool SEL, int TPT, int R>
-void launchForms(const DevicePlan& plan, const NearFast& f, const double* w, double* zp, cudaStream_t st) {
+void launchForms(const DevicePlan& plan, const NearFast& f, const double* w, const ZOut& out, cudaStream_t st) {
   const int tiles = static_cast<int>(plan.nearTilesHost.size()), g = plan.nearGramTileCount;
   FKTB_CUDA(cudaMemsetAsync(plan.dNearCounter.get(), 0, 2 * sizeof(int), st));
   if constexpr (FastKernel<KID>::gram && !SEL)
-    launchStream<KID, D, SEL, TPT, R, true>(plan, f, w, zp, 0, g, plan.dNearCounter.get(), st);
-  launchStream<KID, D, SEL, TPT, R, false>(plan, f, w, zp, g, tiles, plan.dNearCounter.get() + 1, st);
+    launchStream<KID, D, SEL, TPT, R, true>(plan, f, w, out, 0, g, plan.dNearCounter.get(), st);
+  launchStream<KID, D, SEL, TPT, R, false>(plan, f, w, out, g, tiles, plan.dNearCounter.get() + 1, st);
 }
 
 template <int KID, int D, bool SEL, int TPT, int R>
-void launchPasses(const DevicePlan& plan, const NearFast& f, const double* yp, double* zp, int nrhs, cudaStream_t st) {
+void launchPasses(const DevicePlan& plan, const NearFast& f, const double* yp, const ZOut& out, int nrhs, cudaStream_t st) {
   const size_t n = static_cast<size_t>(plan.n);
   const bool fac = plan.dNearFac.get() != nullptr;
   for (int r0 = 0; r0 + R <= nrhs; r0 += R) {
@@ -629,12 +628,12 @@ void launchPasses(const DevicePlan& plan, const NearFast& f, const double* yp, d
       w = plan.dNearW.get();
     }
     FKTB_CUDA(cudaGetLastError());
-    launchForms<KID, D, SEL, TPT, R>(plan, f, w, zp + r0 * n, st);
+    launchForms<KID, D, SEL, TPT, R>(plan, f, w, zoutShift(out, r0), st);
   }
 }
 
 template <int KID, int D, bool SEL>
-void launchFastSel(const DevicePlan& plan, const NearFast& f, const double* yp, double* zp, int nrhs, cudaStream_t st) {
+void launchFastSel(const DevicePlan& plan, const NearFast& f, const double* yp, const ZOut& zp, int nrhs, cudaStream_t st) {
   // targets per lane (measured shapes, B200 sweeps): Matern-3/2 in 3-D 8
   // independent targets; the others 4; 16 RHS: 4 targets x 16 accumulators
   // (each source's 16 weights serve 64 FMAs); 4/8 RHS: 2 targets
@@ -647,7 +646,7 @@ void launchFastSel(const DevicePlan& plan, const NearFast& f, const double* yp, 
 }
 
 template <int KID, int D>
-void launchFastT(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t st) {
+void launchFastT(const DevicePlan& plan, const double* yp, const ZOut& zp, int nrhs, cudaStream_t st) {
   const NearFast f = nearFastConfig<KID>(plan);
   if (f.sel)
     launchFastSel<KID, D, true>(plan, f, yp, zp, nrhs, st);
@@ -717,9 +716,9 @@ template <int KID>
 void launchNearK(const NearArgs& A, const DevicePlan& plan, int tiles, cudaStream_t st) {
   if constexpr (FastKernel<KID>::supported) {
     if (plan.nearRowsBuilt) switch (A.d) {
-      case 2: return launchFastT<KID, 2>(plan, A.yp, A.zp, A.nrhs, st);
-      case 3: return launchFastT<KID, 3>(plan, A.yp, A.zp, A.nrhs, st);
-      case 5: return launchFastT<KID, 5>(plan, A.yp, A.zp, A.nrhs, st);
+      case 2: return launchFastT<KID, 2>(plan, A.yp, A.out, A.nrhs, st);
+      case 3: return launchFastT<KID, 3>(plan, A.yp, A.out, A.nrhs, st);
+      case 5: return launchFastT<KID, 5>(plan, A.yp, A.out, A.nrhs, st);
       default: break;
     }
   }
@@ -802,7 +801,8 @@ void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, 
   const int tiles = static_cast<int>(plan.nearTilesHost.size());
   if (tiles == 0) return;
   const DeviceTree& t = *plan.tree;
-  NearArgs A{t.n, t.d, nrhs, t.pc.get(), t.dBegin.get(), t.dEnd.get(), plan.dNearTiles.get(), t.dNearPos.get(), yp, zp, {}};
+  NearArgs A{t.n, t.d, nrhs, t.pc.get(), t.dBegin.get(), t.dEnd.get(), plan.dNearTiles.get(), t.dNearPos.get(), yp,
+             zoutFor(plan, zp, nrhs, false), {}};
   fillKernelDesc(plan.kernel, A.kd);
   if (plan.options.hasDiagonal) A.kd.diag = plan.options.diagonal;
   switch (plan.kernel.id) {

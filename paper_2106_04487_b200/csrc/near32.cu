@@ -56,7 +56,7 @@ struct Args32 {
   const FktbTile* tiles;
   const uint32_t* nearPos;
   const double* yp;
-  double* zp;
+  ZOut out;
   double sc, wf;
   float diagCanon;
   int sel;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(THREADS) near_fp32(const __grid_constant__ Arg
     for (int i = 0; i < TPT; ++i)
       if (tpos[i] >= 0)
 #pragma unroll
-        for (int r = 0; r < R; ++r) atomicAdd(A.zp + static_cast<size_t>(r0 + r) * n + tpos[i], accd[i][r]);
+        for (int r = 0; r < R; ++r) A.out.add(r0 + r, tile.start + threadIdx.x + i * THREADS, tpos[i], accd[i][r]);
   }
 }
 
@@ -191,7 +191,7 @@ bool launchNear32(const DevicePlan& plan, const double* yp, double* zp, int nrhs
   fillKernelDesc(plan.kernel, kd);
   if (plan.options.hasDiagonal) kd.diag = plan.options.diagonal;
   Args32 A{t.n, t.d, nrhs, t.pc.get(), t.dCenter.get(), t.dBegin.get(), t.dEnd.get(), plan.dNearTiles.get(),
-           t.dNearPos.get(), yp, zp, 1.0, 1.0, 0.0f, 0};
+           t.dNearPos.get(), yp, zoutFor(plan, zp, nrhs, false), 1.0, 1.0, 0.0f, 0};
   switch (kd.id) {
     case FKTB_KERNEL_MATERN32: A.sc = kd.a; A.wf = kd.s2; break;
     case FKTB_KERNEL_MATERN12: A.sc = 1.0 / kd.rho; A.wf = kd.s2; break;

@@ -20,6 +20,7 @@ namespace fktb {
 int nearTileSize();
 int farTileSize();
 int genericGMax();
+int s2mRhsChunk(int P);
 
 namespace {
 
@@ -265,7 +266,9 @@ void buildMomentPlan(DevicePlan& plan) {
   uploadVec(plan.dFarNodes, plan.farNodesHost, st);
   // top levels by composite shifts from the depth-m2mTop frontier (moments.cu
   // m2m_pairs): one launch instead of one latency-bound launch per level
-  const int topDepth = 8;  // B200 sweep 0/6/8/10 (cfg2 S2M 0.294/0.245/0.233/0.248 ms)
+  // (deterministic mode: 0 -- the composite shifts add into a node from
+  // several frontier nodes with atomics; the per-level M2M writes once)
+  const int topDepth = plan.options.deterministic ? 0 : 8;  // B200 sweep 0/6/8/10 (cfg2 S2M 0.294/0.245/0.233/0.248 ms)
   plan.m2mTop = std::min(topDepth, maxDepth);
   std::vector<int> topPairs;
   for (int b = 0; b < t.nodes; ++b) {
@@ -289,16 +292,18 @@ void buildMomentPlan(DevicePlan& plan) {
   buildP2MTiles(plan);
 }
 
-// Leaf tiles of the monomial S2M over the owned sources.
+// Leaf tiles of the monomial S2M over the owned sources (deterministic mode:
+// one tile per leaf, so each leaf's moments have a single writer).
 void buildP2MTiles(DevicePlan& plan) {
   const DeviceTree& t = *plan.tree;
+  const long long tileLen = plan.options.deterministic ? (1ll << 30) : 4096;
   plan.p2mTilesHost.clear();
   for (int b = 0; b < t.nodes; ++b) {
     if (t.left[static_cast<size_t>(b)] >= 0) continue;
     const long long s0 = std::max<long long>(t.begin[static_cast<size_t>(b)], plan.shardLo);
     const long long s1 = std::min<long long>(t.end[static_cast<size_t>(b)], plan.shardHi);
-    for (long long s = s0; s < s1; s += 4096)
-      plan.p2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(4096, s1 - s)), s});
+    for (long long s = s0; s < s1; s += tileLen)
+      plan.p2mTilesHost.push_back(FktbTile{b, static_cast<int>(std::min<long long>(tileLen, s1 - s)), s});
   }
   uploadVec(plan.dP2mTiles, plan.p2mTilesHost, plan.stream);
 }
@@ -355,6 +360,13 @@ void ensureWorkspace(DevicePlan& plan, int nrhs) {
     if (plan.dNearCounter.size() == 0) plan.dNearCounter.resize(2);
   }
   plan.dMoments.resize(std::max<size_t>(1, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs));
+  if (plan.options.deterministic) {
+    // + one all-zero row: the padding slots of the per-target sums read it
+    plan.dPart.resize(static_cast<size_t>(plan.slotsTotal + 1) * nrhs);
+    FKTB_CUDA(cudaMemset(plan.dPart.get() + static_cast<size_t>(plan.slotsTotal) * nrhs, 0, nrhs * sizeof(double)));
+    plan.dZf.resize(n * nrhs);
+    if (!plan.useMoments) plan.dTilePart.resize(std::max<size_t>(1, detTilePartSize(plan, nrhs)));
+  }
   plan.nrhsCap = nrhs;
 }
 
@@ -364,6 +376,10 @@ void rebuildTiles(DevicePlan& plan) {
   clearGraphs(plan);
   buildTiles(plan);
   if (plan.useMoments) buildP2MTiles(plan);
+  if (plan.options.deterministic) {
+    buildDetTileRanges(plan);
+    if (!plan.useMoments && plan.nrhsCap > 0) plan.dTilePart.resize(std::max<size_t>(1, detTilePartSize(plan, plan.nrhsCap)));
+  }
   FKTB_CUDA(cudaStreamSynchronize(plan.stream));
 }
 
@@ -442,6 +458,10 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
   }
   phase(kPhaseMoments);
+  if (options.deterministic) {
+    buildDeterministic(*plan);
+    buildDetTileRanges(*plan);
+  }
   plan->dX.resize(static_cast<size_t>(n) * d);
   FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
@@ -491,6 +511,11 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs) {
     k += plan.options.nearPrecision == 32 ? 1 : nearLaunches(plan, nrhs);
   }
   k += !plan.farTilesHost.empty();
+  if (plan.options.deterministic) {
+    k += 2;  // the far and near sums of the partials
+    if (!plan.useMoments && plan.detTileNodes > 0)  // per-tile S2M partials, per RHS chunk
+      k += plan.options.barnesHut ? 1 : (nrhs + s2mRhsChunk(plan.P) - 1) / s2mRhsChunk(plan.P);
+  }
   return k;
 }
 
@@ -522,8 +547,10 @@ void enqueuePass(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStr
   launchS2MAny(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
   launchNearAny(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);
   launchM2T(plan, plan.dMoments.get(), plan.dZp.get(), nrhs, plan.side);
+  if (plan.options.deterministic) launchDetReduce(plan, nullptr, nrhs, true, plan.side);  // z_far, behind the near field
   FKTB_CUDA(cudaEventRecord(plan.evFar, plan.side));
   FKTB_CUDA(cudaStreamWaitEvent(st, plan.evFar, 0));
+  if (plan.options.deterministic) launchDetReduce(plan, plan.dZp.get(), nrhs, false, st);
   launchScatterZ(plan, plan.dZp.get(), z, nrhs, st);
 }
 

@@ -113,6 +113,12 @@ struct PlanOptions {
   bool hasDiagonal = false;
   double diagonal = 0.0;
   int nearPrecision = 64;  // 64: FP64 near field; 32: FP32 fast mode (near32.cu)
+  bool deterministic = false;  // bitwise reproducible z (det.cu)
+};
+
+struct DetIndex {
+  DeviceBuffer<uint32_t> idx;
+  DeviceBuffer<long long> groupOff;
 };
 
 struct DevicePlan {
@@ -191,6 +197,16 @@ struct DevicePlan {
       graphs;
   unsigned long long graphClock = 0;
   bool useGraphs = true;
+  // Deterministic mode (det.cu): per list, the per-target index into the
+  // partials (sliced by groups of 32 targets, group offsets); the partials of
+  // one pass ([entry][rhs], slotsTotal = near + far entries), z_far, the
+  // per-tile S2M partials and their node ranges.
+  bool detBuilt = false;
+  long long slotsTotal = 0;
+  DetIndex detNear, detFar;
+  DeviceBuffer<double> dPart, dTilePart, dZf;
+  DeviceBuffer<int> dDetTileRanges;
+  int detTileNodes = 0;
 };
 
 enum { kPhaseTree = 0, kPhaseSets, kPhaseTables, kPhaseTiles, kPhaseNearRows, kPhaseMoments, kPhaseOther, kPhaseCount };
@@ -230,6 +246,17 @@ long long kernelLaunches(const DevicePlan& plan, int nrhs);
 void buildBarnesHut(DevicePlan& plan);
 void launchBHSums(const DevicePlan& plan, const double* yp, double* totals, int nrhs, cudaStream_t stream);
 void launchBHFar(const DevicePlan& plan, const double* totals, double* zp, int nrhs, cudaStream_t stream);
+
+// Deterministic mode (det.cu).
+void buildDeterministic(DevicePlan& plan);
+void buildDetTileRanges(DevicePlan& plan);
+ZOut zoutFor(const DevicePlan& plan, double* zp, int nrhs, bool far);
+ZOut zoutShift(ZOut o, int r0);
+// far = true: z_far from the far partials; false: zp = z_far + the near partials
+void launchDetReduce(const DevicePlan& plan, double* zp, int nrhs, bool far, cudaStream_t stream);
+void launchDetTileSum(const DevicePlan& plan, const double* part, int PC, int nrhs, double* moments, cudaStream_t stream);
+// per-tile S2M partials one launch of nrhs right-hand sides needs (doubles)
+size_t detTilePartSize(const DevicePlan& plan, int nrhs);
 
 void launchNear(const DevicePlan& plan, const double* yp, double* zp, int nrhs, cudaStream_t stream);
 // Streaming near field: plan-time rows and tile order (near.cu); launches
