@@ -51,13 +51,14 @@ def near_flops_per_pair(kernel: str, d: int) -> int:
 
 
 # FP64 work the near kernel actually executes per (target, source) pair, from
-# the SASS of its inner pair loop (scripts/sass_loops.py on build/near.o; the
-# pair covers all right-hand sides): (FP64 instructions, flops with FMA = 2).
+# the SASS of its inner pair loop (scripts/sass_pair_mix.py on build/near.o,
+# profiles/r02_sass_near_pairs.txt; the pair covers all right-hand sides):
+# (FP64 instructions, flops with FMA = 2).
 # The SURVEY §8(d) convention above charges exp = 20, sqrt / div = 8 flops;
 # the fast-math bodies need fewer, so the convention-based
 # roofline.frac can exceed 1 while the FP64 pipe is ~70% busy.
 EXEC_FP64_PER_PAIR = {
-    ("matern32", 3, 1): (16, 27),   # Gram form: 11 DFMA, 3 DMUL, 2 DADD
+    ("matern32", 3, 1): (15, 26),   # Gram form: 11 DFMA, 2 DMUL, 2 DADD
     ("gaussian", 5, 1): (12, 22),   # factored Gram form: 10 DFMA, 1 DMUL, 1 DADD
     ("inverse-r", 3, 1): (10, 16),  # difference form + select: 6 DFMA, 1 DMUL, 3 DADD
     ("cauchy", 2, 16): (23, 45),    # Gram form, 16 RHS: 22 DFMA, 1 DADD
@@ -300,6 +301,22 @@ def run_ours(args):
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # the drop-in FktPlan::multiply(std::span) path: PAGEABLE host buffers
+    # (numpy, like std::vector) through the same C-ABI call
+    pageable_s = None
+    if not sharded:
+        ya = np.array(yh.numpy(), copy=True)
+        za = np.empty_like(ya)
+
+        def page_mul():
+            fkt._check(fkt.lib.fkt_plan_multiply(pl._h, ya.ctypes.data_as(C.POINTER(C.c_double)),
+                                                 za.ctypes.data_as(C.POINTER(C.c_double)), nrhs))
+
+        page_mul()
+        tp = time.perf_counter()
+        for _ in range(e2e_steps):
+            page_mul()
+        pageable_s = (time.perf_counter() - tp) / e2e_steps
 
     launches = int(fkt.lib.fkt_plan_kernel_launches(pl._h, nrhs))
     shard_lo, shard_hi = pl.shard_range()
@@ -387,7 +404,12 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(zh.numel() * 8) * world,
                 "method": ("ShardedPlan.multiply_device per rank (pinned host y -> H2D, sharded MVM, D2H of all z), "
                            "wall clock, max over ranks" if sharded else
-                           "fkt_plan_multiply (C-ABI, pinned host y/z, H2D+MVM+D2H per step), wall clock")},
+                           "fkt_plan_multiply (C-ABI, pinned host y/z, H2D+MVM+D2H per step), wall clock"),
+                "pageable": (None if pageable_s is None else
+                             {"value": 1.0 / pageable_s, "unit": "MVM/s",
+                              "method": "fkt_plan_multiply on pageable host buffers (numpy; what FktPlan::multiply"
+                                        "(std::span) with std::vector storage runs): chunked staging through "
+                                        "pinned bounce buffers, wall clock"})},
         "gpu_launches": launches * args.steps,
         "gpu_launches_per_step": launches,
         "clocks": clocks.summary(),

@@ -377,15 +377,7 @@ int fkt_plan_multiply(fkt_plan_t plan, const double* y, double* z, int nrhs) {
     if (nrhs < 1) throw DimensionMismatch("multiply: nrhs must be >= 1");
     auto& p = *plan->plan;
     std::lock_guard<std::mutex> lock(p.mutex);
-    const size_t bytes = static_cast<size_t>(p.n) * nrhs * sizeof(double);
-    if (p.dYio.size() < static_cast<size_t>(p.n) * nrhs) {
-      p.dYio.resize(static_cast<size_t>(p.n) * nrhs);
-      p.dZio.resize(static_cast<size_t>(p.n) * nrhs);
-    }
-    FKTB_CUDA(cudaMemcpyAsync(p.dYio.get(), y, bytes, cudaMemcpyHostToDevice, p.stream));
-    fktb::multiplyDevice(p, p.dYio.get(), p.dZio.get(), nrhs, p.stream);
-    FKTB_CUDA(cudaMemcpyAsync(z, p.dZio.get(), bytes, cudaMemcpyDeviceToHost, p.stream));
-    FKTB_CUDA(cudaStreamSynchronize(p.stream));
+    fktb::multiplyHost(p, y, z, nrhs);
   });
 }
 

@@ -10,18 +10,23 @@
 namespace fktb {
 namespace {
 
-__global__ void gather_y(const double* y, const uint32_t* order, double* yp, int n, int nrhs) {
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= static_cast<long long>(n) * nrhs) return;
-  const long long r = i / n, pos = i % n;
-  yp[i] = y[r * n + order[pos]];
+// grid (positions / 256, right-hand sides): coalesced on the tree-order side;
+// the original-order side is a permutation (a column stays L2-resident at the
+// BASELINE sizes). 32-bit index math (no 64-bit division per element).
+__global__ void gather_y(const double* __restrict__ y, const uint32_t* __restrict__ order, double* __restrict__ yp,
+                         int n) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const size_t col = static_cast<size_t>(blockIdx.y) * n;
+  yp[col + pos] = y[col + order[pos]];
 }
 
-__global__ void scatter_z(const double* zp, const uint32_t* order, double* z, int n, int nrhs) {
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= static_cast<long long>(n) * nrhs) return;
-  const long long r = i / n, pos = i % n;
-  z[r * n + order[pos]] = zp[i];
+__global__ void scatter_z(const double* __restrict__ zp, const uint32_t* __restrict__ order, double* __restrict__ z,
+                          int n) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const size_t col = static_cast<size_t>(blockIdx.y) * n;
+  z[col + order[pos]] = zp[col + pos];
 }
 
 constexpr int kDenseThreads = 128;
@@ -99,14 +104,12 @@ void launchDense(const DenseArgs& A, cudaStream_t st) {
 }  // namespace
 
 void launchGatherY(const DevicePlan& plan, const double* y, double* yp, int nrhs, cudaStream_t st) {
-  const long long tot = static_cast<long long>(plan.n) * nrhs;
-  gather_y<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(y, plan.tree->order.get(), yp, plan.n, nrhs);
+  gather_y<<<dim3((plan.n + 255) / 256, nrhs), 256, 0, st>>>(y, plan.tree->order.get(), yp, plan.n);
   FKTB_CUDA(cudaGetLastError());
 }
 
 void launchScatterZ(const DevicePlan& plan, const double* zp, double* z, int nrhs, cudaStream_t st) {
-  const long long tot = static_cast<long long>(plan.n) * nrhs;
-  scatter_z<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(zp, plan.tree->order.get(), z, plan.n, nrhs);
+  scatter_z<<<dim3((plan.n + 255) / 256, nrhs), 256, 0, st>>>(zp, plan.tree->order.get(), z, plan.n);
   FKTB_CUDA(cudaGetLastError());
 }
 

@@ -480,6 +480,7 @@ void destroyPlan(DevicePlan* plan) {
   cudaStream_t st = plan->stream, side = plan->side;
   cudaEvent_t e0 = plan->evGather, e1 = plan->evFar, e2 = plan->evDone;
   if (plan->doneRecorded) cudaEventSynchronize(e2);
+  releaseHostIo(*plan);
   clearGraphs(*plan);
   delete plan;
   if (st) cudaStreamDestroy(st);

@@ -140,6 +140,13 @@ struct DevicePlan {
   DeviceBuffer<double> dX;               // original coordinates, row-major (dense paths)
   DeviceBuffer<double> dYp, dZp;         // permuted workspaces (n x nrhsCap)
   DeviceBuffer<double> dYio, dZio;       // staging for host-buffer multiplies
+  // host-buffer multiplies (hostio.cu): copy streams, group events, pinned
+  // bounce buffers for pageable y / z
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t evIo[4] = {};
+  void* bounceIn = nullptr;
+  void* bounceOut = nullptr;
+  size_t bounceBytes = 0;
   int nrhsCap = 0;
   double planSeconds = 0.0;
   // plan-time phases (seconds): tree, sets, exact tables, tiles, near rows,
@@ -216,6 +223,9 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
 void destroyPlan(DevicePlan* plan);
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
+// z = K y on host buffers (pinned or pageable), synchronous (hostio.cu).
+void multiplyHost(DevicePlan& plan, const double* y, double* z, int nrhs);
+void releaseHostIo(DevicePlan& plan);
 
 // 2^(j/2^bits), j < 2^bits, in device memory (default 64 entries: the far
 // kernels; the near field uses kNearExpBits).
