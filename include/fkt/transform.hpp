@@ -69,6 +69,10 @@ class FktPlan {
   // Device buffers (n * nrhs doubles each) on a cudaStream_t (nullptr: the
   // plan's own stream, synchronised before return).
   void multiplyDevice(const double* yDevice, double* zDevice, int nrhs = 1, void* stream = nullptr) const;
+  // Additive: the same plan on new coordinates of the same n points (moving
+  // points); equals FktPlan(cloud, kernel(), options()), reusing the plan's
+  // device buffers. DimensionMismatchError on a different n or d.
+  void rebuild(PointCloud cloud);
 
   const PointCloud& cloud() const { return cloud_; }
   const PartitionTree& tree() const;

@@ -92,6 +92,13 @@ void fkt_default_options(fkt_options* opt);
 int fkt_plan_create(int n, int d, const double* x, const char* kernel, const char* const* keys,
                     const double* values, int nparams, const fkt_options* opt, fkt_plan_t* out);
 int fkt_plan_destroy(fkt_plan_t plan);
+/* Additive (no reference counterpart; the reference rebuilds FktPlan from a
+ * new PointCloud, transform.cpp:39-92): the same plan on new coordinates of
+ * the same n points, x host row-major n x d. Tree, interaction sets, tiles and
+ * moment plan are rebuilt on the GPU reusing the plan's buffers; the result
+ * equals fkt_plan_create on x with the plan's kernel and options. Cached plans
+ * (fkt_plan_cache_get) are shared and refuse it. */
+int fkt_plan_rebuild(fkt_plan_t plan, const double* x);
 int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info);
 
 /* Plan cache (the reference rebuilds a plan per call site, e.g.

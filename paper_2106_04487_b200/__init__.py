@@ -395,6 +395,22 @@ class FktPlan:
     def close(self):
         self.__del__()
 
+    def rebuild(self, cloud) -> None:
+        """Additive: the same plan on new coordinates of the same n points
+        (moving points, e.g. t-SNE iterations). Equals a fresh plan on `cloud`
+        with this plan's kernel and options; tree, sets, tiles and moment plan
+        are rebuilt on the GPU reusing the plan's buffers (fkt_plan_rebuild)."""
+        x = cloud.x if isinstance(cloud, PointCloud) else np.asarray(cloud, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim != 2 or x.shape != (self._cloud.n, self._cloud.d):
+            raise DimensionMismatchError("rebuild: the cloud must have the plan's n points in d dimensions")
+        _check(lib.fkt_plan_rebuild(self._h, _dptr(x)))
+        self._cloud = PointCloud(self._cloud.n, self._cloud.d, x.copy())
+        self._tree = None
+        info = _L.FktPlanInfoC()
+        _check(lib.fkt_plan_info_get(self._h, C.byref(info)))
+        self._info = info
+
     # reference accessors
     def cloud(self) -> PointCloud:
         return self._cloud

@@ -95,6 +95,7 @@ SIGNATURES = {
     "fkt_plan_create": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int,
                         C.POINTER(FktOptionsC), C.POINTER(C.c_void_p)),
     "fkt_plan_destroy": (C.c_int, C.c_void_p),
+    "fkt_plan_rebuild": (C.c_int, C.c_void_p, _d),
     "fkt_plan_cache_get": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int, C.POINTER(FktOptionsC),
                            C.POINTER(C.c_void_p), _i32),
     "fkt_plan_cache_release": (C.c_int, C.c_void_p),

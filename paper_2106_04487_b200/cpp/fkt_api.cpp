@@ -296,6 +296,14 @@ std::vector<double> FktPlan::multiply(std::span<const double> y, int nrhs) const
   return z;
 }
 
+void FktPlan::rebuild(PointCloud cloud) {
+  if (cloud.n != cloud_.n || cloud.d != cloud_.d)
+    throw DimensionMismatchError("rebuild: the cloud must have the plan's n points in d dimensions");
+  check(fkt_plan_rebuild(static_cast<fkt_plan_t>(h_), cloud.x.data()));
+  cloud_ = std::move(cloud);
+  tree_.reset();
+}
+
 void FktPlan::multiplyDevice(const double* y, double* z, int nrhs, void* stream) const {
   check(fkt_plan_multiply_device(static_cast<fkt_plan_t>(h_), y, z, nrhs, stream));
 }

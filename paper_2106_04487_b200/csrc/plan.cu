@@ -428,7 +428,11 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     tPrev = now;
   };
   plan->tree = std::make_unique<DeviceTree>();
-  buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream);
+  // one H2D of the coordinates (row-major, kept for the dense paths); the
+  // tree is built from the device copy
+  plan->dX.resize(static_cast<size_t>(n) * d);
+  FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
+  buildTreeGpu(*plan->tree, hostX, n, d, options.leafCapacity, plan->stream, plan->dX.get());
   phase(kPhaseTree);
   computeSetsGpu(*plan->tree, options.theta);
   phase(kPhaseSets);
@@ -462,15 +466,66 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
     buildDeterministic(*plan);
     buildDetTileRanges(*plan);
   }
-  plan->dX.resize(static_cast<size_t>(n) * d);
-  FKTB_CUDA(cudaMemcpyAsync(plan->dX.get(), hostX, plan->dX.bytes(), cudaMemcpyHostToDevice, plan->stream));
   ensureWorkspace(*plan, 1);
   (void)expTableDevice();  // lazy device tables: initialise outside any graph capture
   (void)expTableDevice(kNearExpBits, true);
   if (const char* g = std::getenv("FKTB_GRAPHS")) plan->useGraphs = std::atoi(g) != 0;
+  plan->tree->scratch = DeviceTree::Scratch{};  // lean plans: rebuildPlan re-sizes it on demand
   phase(kPhaseOther);
   plan->planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return plan;
+}
+
+// Moving points (t-SNE-style iterations): the same plan on new coordinates of
+// the same n points. Tree, sets, tiles, geometry rows, the moment plan and
+// the shard are rebuilt on the GPU; the kernel tables (T-bar, harmonics,
+// compression) and every buffer are kept, so no cudaMalloc runs once the
+// first rebuild has sized the build scratch. Equals a fresh plan on x.
+void rebuildPlan(DevicePlan& plan, const double* hostX) {
+  const auto t0 = std::chrono::steady_clock::now();
+  FKTB_CUDA(cudaStreamSynchronize(plan.stream));
+  FKTB_CUDA(cudaStreamSynchronize(plan.side));
+  if (plan.doneRecorded) FKTB_CUDA(cudaEventSynchronize(plan.evDone));
+  clearGraphs(plan);
+  for (double& s : plan.phaseSeconds) s = 0.0;
+  auto tPrev = std::chrono::steady_clock::now();
+  auto phase = [&](int i) {
+    FKTB_CUDA(cudaStreamSynchronize(plan.stream));
+    const auto now = std::chrono::steady_clock::now();
+    plan.phaseSeconds[i] += std::chrono::duration<double>(now - tPrev).count();
+    tPrev = now;
+  };
+  DeviceTree& t = *plan.tree;
+  FKTB_CUDA(cudaMemcpyAsync(plan.dX.get(), hostX, plan.dX.bytes(), cudaMemcpyHostToDevice, plan.stream));
+  buildTreeGpu(t, hostX, plan.n, plan.d, plan.options.leafCapacity, plan.stream, plan.dX.get());
+  phase(kPhaseTree);
+  computeSetsGpu(t, plan.options.theta);
+  phase(kPhaseSets);
+  plan.shardLo = 0;
+  plan.shardHi = static_cast<uint32_t>(plan.n);
+  plan.farSub.clear();
+  plan.nearSub.clear();
+  plan.nearRowsBuilt = false;
+  buildTiles(plan);
+  phase(kPhaseTiles);
+  plan.phaseSeconds[kPhaseTiles] -= plan.phaseSeconds[kPhaseNearRows];
+  if (plan.options.barnesHut)
+    buildBarnesHut(plan);
+  else if (plan.useMoments)
+    buildMomentPlan(plan);
+  phase(kPhaseMoments);
+  if (plan.options.deterministic) {
+    buildDeterministic(plan);
+    buildDetTileRanges(plan);
+  }
+  if (plan.shards > 1) setShard(plan, plan.shard, plan.shards);
+  // workspaces sized by the new tree (deterministic partials, S2M tile
+  // partials) at the pass width already in use
+  const int cap = std::max(1, plan.nrhsCap);
+  plan.nrhsCap = 0;
+  ensureWorkspace(plan, cap);
+  phase(kPhaseOther);
+  plan.planSeconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 void destroyPlan(DevicePlan* plan) {

@@ -28,29 +28,41 @@ class DeviceBuffer {
   ~DeviceBuffer() { release(); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_), cap_(o.cap_) {
     o.p_ = nullptr;
-    o.n_ = 0;
+    o.n_ = o.cap_ = 0;
   }
   DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
     if (this != &o) {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      cap_ = o.cap_;
       o.p_ = nullptr;
-      o.n_ = 0;
+      o.n_ = o.cap_ = 0;
     }
     return *this;
   }
+  // Keeps the allocation when it is large enough (re-plans reuse buffers:
+  // cudaMalloc / cudaFree of hundreds of MB synchronise the device and cost
+  // milliseconds); the contents are NOT preserved either way.
+  // A buffer that has to GROW gets 1/8 headroom (list sizes drift between
+  // rebuilds on moving points; the first allocation is exact).
   void resize(std::size_t n) {
+    if (n <= cap_) {
+      n_ = n;
+      return;
+    }
+    const std::size_t c = cap_ ? n + n / 8 : n;
     release();
-    if (n) FKTB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    if (c) FKTB_CUDA(cudaMalloc(&p_, c * sizeof(T)));
     n_ = n;
+    cap_ = c;
   }
   void release() {
     if (p_) cudaFree(p_);
     p_ = nullptr;
-    n_ = 0;
+    n_ = cap_ = 0;
   }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
@@ -58,7 +70,7 @@ class DeviceBuffer {
 
  private:
   T* p_ = nullptr;
-  std::size_t n_ = 0;
+  std::size_t n_ = 0, cap_ = 0;
 };
 
 // Partition tree + interaction sets resident in HBM.
@@ -90,11 +102,25 @@ struct DeviceTree {
   DeviceBuffer<long long> dFarOff, dNearOff;
   DeviceBuffer<uint32_t> dFarPos, dNearPos;
 
+  // Build temporaries kept across rebuilds (fkt_plan_rebuild: same n, d).
+  struct Scratch {
+    DeviceBuffer<double> x, tc, lo, hi, c, r;
+    DeviceBuffer<uint32_t> torder, farNode, farPos, nearNode, nearPos, keysOut;
+    DeviceBuffer<int> segB, segE, mid, narOut, itemLower, itemLowPre, itemUpPre, wideB, wideE, wideOut, segItem;
+    DeviceBuffer<int> farCnt, nearCnt;
+    DeviceBuffer<long long> farStart, nearStart;
+    DeviceBuffer<unsigned char> temp;
+    DeviceBuffer<int4> items;
+    DeviceBuffer<unsigned char> wide;  // WideSeg records
+  } scratch;
+
   cudaStream_t stream = nullptr;
 };
 
 // Build the tree for `x` (row-major n x d, host) on `stream`.
-void buildTreeGpu(DeviceTree& t, const double* hostX, int n, int d, int leafCapacity, cudaStream_t stream);
+// devX: the same coordinates already on the device (row-major), else hostX is copied
+void buildTreeGpu(DeviceTree& t, const double* hostX, int n, int d, int leafCapacity, cudaStream_t stream,
+                  const double* devX = nullptr);
 void computeSetsGpu(DeviceTree& t, double theta);
 
 // Host materialisation of the sets in the reference's form: original point
@@ -221,6 +247,8 @@ enum { kPhaseTree = 0, kPhaseSets, kPhaseTables, kPhaseTiles, kPhaseNearRows, kP
 std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const KernelSpec& kernel,
                                        const PlanOptions& options);
 void destroyPlan(DevicePlan* plan);
+// Same plan, new coordinates of the same n points (moving points).
+void rebuildPlan(DevicePlan& plan, const double* hostX);
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
 // z = K y on host buffers (pinned or pageable), synchronous (hostio.cu).

@@ -281,3 +281,26 @@ def test_unusual_dimensions(fkt, ref, d):
     rp = ref.RefPlan(x, "gaussian", {}, p=3, theta=0.7, leaf=64)
     assert p.coefficientCount() == rp.coef
     assert fkt.relativeError(p.multiply(y), rp.multiply(y)) <= 1e-10
+
+
+def test_wide_levels_edge_cases(fkt, ref):
+    """Segments above 16K points split on the multi-CTA path (tree.cu wide
+    levels): duplicates, ties at the median, the all-on-one-side fallback,
+    zero extent and collinear / clustered clouds at sizes that reach it."""
+    rng = np.random.default_rng(12)
+    x = np.repeat(rng.random((400, 3)), 100, axis=0)  # 40K points, 100 copies each
+    tree_matches_reference(fkt, ref, x, 64, 0.5)
+    grid = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(25.0)), -1).reshape(-1, 3)
+    tree_matches_reference(fkt, ref, grid, 32, 0.5)  # 40K points, heavy ties
+    lop = np.zeros((50000, 3))
+    lop[:45000, 0] = 1.0  # the median equals the max: fallback split below the maximum
+    lop[45000:, 0] = rng.random(5000)
+    lop[:, 1:] = rng.random((50000, 2)) * 1e-3
+    tree_matches_reference(fkt, ref, lop, 128, 0.5)
+    line = np.zeros((60000, 2))
+    line[:, 0] = rng.random(60000)
+    tree_matches_reference(fkt, ref, line, 256, 0.6)
+    same = np.tile(np.array([[0.1, 0.2]]), (30000, 1))  # zero extent: one leaf
+    assert tree_matches_reference(fkt, ref, same, 64, 0.5).nodeCount() == 1
+    clus = np.concatenate([rng.normal(0.2, 1e-4, (40000, 3)), rng.random((20000, 3))])
+    tree_matches_reference(fkt, ref, clus, 100, 0.5)
