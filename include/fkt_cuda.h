@@ -126,7 +126,7 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
 
 /* Multi-GPU target sharding (replaces the node-chunked thread
  * split of FktPlan::multiply, transform.cpp:18-35,184-204). Every rank holds
- * the full plan and owns the contiguous, leaf-aligned, cost-balanced range
+ * the full plan and owns the contiguous, cost-balanced range
  * [pos_lo, pos_hi) of tree positions. Under a shard, multiply computes
  *   stage 1: partial node moments from the owned sources only,
  *   stage 2/3: near and far interactions of the owned targets only,
@@ -135,6 +135,20 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
  * exchange; fkt_plan_moments_device exposes the table, [rhs][node][P], count =
  * nodes * P per right-hand side). shards = 1 restores the whole problem. */
 int fkt_plan_set_shard(fkt_plan_t plan, int shard, int shards);
+/* The whole sharded MVM in one call (csrc/multigpu.cu): gather, S2M of the
+ * owned sources, NCCL all-reduce of the moments, near + M2T of the owned
+ * targets, NCCL broadcast of every rank's owned z range, scatter -- all of z
+ * on every rank, captured as one CUDA graph per (y, z, nrhs, stream). The plan
+ * must be set to shard (rank, size) of the communicator. nccl_comm: an
+ * ncclComm_t, e.g. from fkt_nccl_comm_create; NCCL is loaded at run time
+ * (libnccl.so.2), FKT_ERR_UNSUPPORTED when it is not loadable. */
+int fkt_plan_multiply_sharded(fkt_plan_t plan, const double* y_dev, double* z_dev, int nrhs, void* nccl_comm,
+                              void* stream);
+/* NCCL communicator helpers: rank 0 makes a 128-byte id, every rank passes it
+ * (shared over any side channel, e.g. torch.distributed) to comm_create. */
+int fkt_nccl_unique_id(char* id128);
+int fkt_nccl_comm_create(const char* id128, int nranks, int rank, void** comm);
+int fkt_nccl_comm_destroy(void* comm);
 int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi);
 int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_per_rhs);
 /* Near-field tiles (leaf, <= 256 targets) of the FP64 near field, and how many

@@ -501,7 +501,7 @@ class FktPlan:
 
     # ---- multi-GPU target sharding (see distributed.py) ----------
     def set_shard(self, shard: int, shards: int) -> None:
-        """Own the cost-balanced, leaf-aligned target range `shard` of `shards`."""
+        """Own the cost-balanced target range `shard` of `shards` (tree positions)."""
         _check(lib.fkt_plan_set_shard(self._h, int(shard), int(shards)))
 
     def shard_range(self):

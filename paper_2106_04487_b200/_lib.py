@@ -96,6 +96,10 @@ SIGNATURES = {
                         C.POINTER(FktOptionsC), C.POINTER(C.c_void_p)),
     "fkt_plan_destroy": (C.c_int, C.c_void_p),
     "fkt_plan_rebuild": (C.c_int, C.c_void_p, _d),
+    "fkt_plan_multiply_sharded": (C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p),
+    "fkt_nccl_unique_id": (C.c_int, C.c_char_p),
+    "fkt_nccl_comm_create": (C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)),
+    "fkt_nccl_comm_destroy": (C.c_int, C.c_void_p),
     "fkt_plan_cache_get": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int, C.POINTER(FktOptionsC),
                            C.POINTER(C.c_void_p), _i32),
     "fkt_plan_cache_release": (C.c_int, C.c_void_p),

@@ -448,6 +448,34 @@ int fkt_plan_set_shard(fkt_plan_t plan, int shard, int shards) {
   });
 }
 
+int fkt_plan_multiply_sharded(fkt_plan_t plan, const double* y_dev, double* z_dev, int nrhs, void* nccl_comm,
+                              void* stream) {
+  return guarded([&] {
+    if (nrhs < 1) throw DimensionMismatch("multiply: nrhs must be >= 1");
+    if (!nccl_comm) throw std::invalid_argument("sharded multiply: null communicator");
+    auto& p = *plan->plan;
+    std::lock_guard<std::mutex> lock(p.mutex);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    fktb::multiplySharded(p, y_dev, z_dev, nrhs, nccl_comm, st);
+    if (!stream) FKTB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fkt_nccl_unique_id(char* id128) {
+  return guarded([&] { fktb::ncclUniqueIdBytes(id128); });
+}
+
+int fkt_nccl_comm_create(const char* id128, int nranks, int rank, void** comm) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("nccl comm: 0 <= rank < nranks");
+    *comm = fktb::ncclCommCreate(id128, nranks, rank);
+  });
+}
+
+int fkt_nccl_comm_destroy(void* comm) {
+  return guarded([&] { fktb::ncclCommRelease(comm); });
+}
+
 int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi) {
   return guarded([&] {
     *pos_lo = plan->plan->shardLo;

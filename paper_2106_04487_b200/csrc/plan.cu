@@ -204,6 +204,7 @@ void buildTiles(DevicePlan& plan) {
 void clearGraphs(DevicePlan& plan) {
   for (auto& kv : plan.graphs) cudaGraphExecDestroy(kv.second.first);
   plan.graphs.clear();
+  clearShardedGraphs(plan);
 }
 
 template <class T>
@@ -390,6 +391,7 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   plan->n = n;
   plan->d = d;
   plan->shardHi = static_cast<uint32_t>(n);
+  plan->cuts = {0u, static_cast<uint32_t>(n)};
   plan->options = options;
   plan->kernel = kernel;
   if (options.barnesHut) plan->options.p = 0;  // transform.cpp:44
@@ -503,6 +505,7 @@ void rebuildPlan(DevicePlan& plan, const double* hostX) {
   phase(kPhaseSets);
   plan.shardLo = 0;
   plan.shardHi = static_cast<uint32_t>(plan.n);
+  plan.cuts = {0u, static_cast<uint32_t>(plan.n)};
   plan.farSub.clear();
   plan.nearSub.clear();
   plan.nearRowsBuilt = false;

@@ -217,6 +217,7 @@ struct DevicePlan {
   // (empty = whole lists).
   int shard = 0, shards = 1;
   uint32_t shardLo = 0, shardHi = 0;
+  std::vector<uint32_t> cuts;  // every rank's range: [cuts[r], cuts[r + 1])
   std::vector<long long> farSub, nearSub;
   // Barnes-Hut plans (bh.cu): per-node centres of mass, nodes x d.
   DeviceBuffer<double> dCom;
@@ -230,6 +231,8 @@ struct DevicePlan {
       graphs;
   unsigned long long graphClock = 0;
   bool useGraphs = true;
+  // sharded multiplies (multigpu.cu): graph per (y, z, nrhs, stream) with its communicator
+  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, std::pair<cudaGraphExec_t, void*>> shardedGraphs;
   // Deterministic mode (det.cu): per list, the per-target index into the
   // partials (sliced by groups of 32 targets, group offsets); the partials of
   // one pass ([entry][rhs], slotsTotal = near + far entries), z_far, the
@@ -249,6 +252,13 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
 void destroyPlan(DevicePlan* plan);
 // Same plan, new coordinates of the same n points (moving points).
 void rebuildPlan(DevicePlan& plan, const double* hostX);
+// Multi-GPU (multigpu.cu): NCCL communicators (dlopen'd libnccl) and the
+// sharded MVM with both exchanges in one graph.
+void ncclUniqueIdBytes(char* out128);
+void* ncclCommCreate(const char* idBytes, int nranks, int rank);
+void ncclCommRelease(void* comm);
+void multiplySharded(DevicePlan& plan, const double* y, double* z, int nrhs, void* comm, cudaStream_t stream);
+void clearShardedGraphs(DevicePlan& plan);
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
 // z = K y on host buffers (pinned or pageable), synchronous (hostio.cu).

@@ -3,7 +3,7 @@
 // The reference MVM (transform.cpp:184-204) splits work over CPU threads by
 // node chunks and merges per-thread z. Across GPUs the natural split is by
 // TARGET: every rank holds the full plan (tree, sets, tables; cheap), owns a
-// contiguous, leaf-aligned range [lo, hi) of tree positions, and
+// contiguous, cost-balanced range [lo, hi) of tree positions, and
 //   1. S2M: builds partial node moments from the sources it owns,
 //   2. exchange: sum of the moment tables over ranks (nodes x P doubles;
 //      3 MB at cfg2) -- the only data-path collective,
@@ -18,6 +18,8 @@
 // Cut placement balances an estimated per-target cost: a near pair (t, leaf l)
 // costs |l| kernel evaluations; a far pair (t, node) costs farPairWeight(P)
 // evaluations (measured on cfg2: one M2T pair ~ 17 near evaluations at P=84).
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <numeric>
 
@@ -83,18 +85,32 @@ std::vector<uint32_t> shardCuts(const DeviceTree& t, int P, int shards) {
   shard_cost_kernel<<<t.nodes, 256, 0, t.stream>>>(t.dFarOff.get(), t.dFarPos.get(), t.dBegin.get(), t.dEnd.get(), 0,
                                                    farPairWeight(P), dCost.get());
   FKTB_CUDA(cudaGetLastError());
-  std::vector<unsigned long long> cost(static_cast<size_t>(n));
-  FKTB_CUDA(cudaMemcpyAsync(cost.data(), dCost.get(), dCost.bytes(), cudaMemcpyDeviceToHost, t.stream));
-  FKTB_CUDA(cudaStreamSynchronize(t.stream));
-  // leaves in position order (pre-order visits left before right)
-  std::vector<std::pair<uint32_t, unsigned long long>> leafEnd;  // (end position, cumulative cost)
-  unsigned long long acc = 0;
-  for (int b = 0; b < t.nodes; ++b) {
-    if (t.left[static_cast<size_t>(b)] >= 0) continue;
-    for (uint32_t p = t.begin[static_cast<size_t>(b)]; p < t.end[static_cast<size_t>(b)]; ++p) acc += cost[p];
-    leafEnd.emplace_back(t.end[static_cast<size_t>(b)], acc);
+  // cumulative cost over tree positions; cuts at any position (not only leaf
+  // boundaries: a leaf split between ranks just has its sources' moments
+  // summed by the exchange and its near list sub-ranged by target)
+  DeviceBuffer<unsigned long long> dCum(static_cast<size_t>(n));
+  {
+    size_t bytes = 0;
+    FKTB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, dCost.get(), dCum.get(), n, t.stream));
+    DeviceBuffer<unsigned char> temp(bytes + 1);
+    FKTB_CUDA(cub::DeviceScan::InclusiveSum(temp.get(), bytes, dCost.get(), dCum.get(), n, t.stream));
+    FKTB_CUDA(cudaStreamSynchronize(t.stream));
   }
-  return shardCutsFromLeaves(leafEnd, shards, static_cast<uint32_t>(n));
+  std::vector<unsigned long long> cum(static_cast<size_t>(n));
+  FKTB_CUDA(cudaMemcpyAsync(cum.data(), dCum.get(), dCum.bytes(), cudaMemcpyDeviceToHost, t.stream));
+  FKTB_CUDA(cudaStreamSynchronize(t.stream));
+  const unsigned long long total = cum.back();
+  for (int s = 1; s < shards; ++s) {
+    // the boundary after position p carries cum[p]: the one closest to s/shards of the total
+    const double goal = static_cast<double>(total) * s / shards;
+    size_t p = static_cast<size_t>(std::lower_bound(cum.begin(), cum.end(), static_cast<unsigned long long>(goal)) -
+                                   cum.begin());
+    if (p >= static_cast<size_t>(n)) p = static_cast<size_t>(n) - 1;
+    uint32_t c = static_cast<uint32_t>(p + 1);
+    if (p > 0 && goal - static_cast<double>(cum[p - 1]) < static_cast<double>(cum[p]) - goal) c = static_cast<uint32_t>(p);
+    cuts[static_cast<size_t>(s)] = std::max(c, cuts[static_cast<size_t>(s) - 1]);
+  }
+  return cuts;
 }
 
 std::vector<uint32_t> shardCutsFromLeaves(const std::vector<std::pair<uint32_t, unsigned long long>>& leafEnd, int shards,
@@ -127,6 +143,7 @@ void setShard(DevicePlan& plan, int shard, int shards) {
   plan.shards = shards;
   plan.shardLo = cuts[static_cast<size_t>(shard)];
   plan.shardHi = cuts[static_cast<size_t>(shard) + 1];
+  plan.cuts = cuts;
   if (shards == 1) {
     plan.farSub.clear();
     plan.nearSub.clear();

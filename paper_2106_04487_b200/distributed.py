@@ -3,7 +3,7 @@
 The reference parallelises one MVM over CPU threads by chunks of nodes, each
 thread with its own z, merged in order (transform.cpp:18-35, 184-204). Here
 one process per GPU holds the full plan (tree, sets and tables are cheap to
-replicate) and owns a contiguous, leaf-aligned, cost-balanced range of tree
+replicate) and owns a contiguous, cost-balanced range of tree
 positions (fkt_plan_set_shard, csrc/shard.cu). One MVM is then
 
     stage 0  gather y into tree order              (every rank, all of y)
@@ -18,12 +18,19 @@ Moments and z are sums of per-rank partials; non-owned z entries are exact
 zeros, so the z sum is exact and the only rounding difference from one GPU is
 the order of the moment sum (~1e-16 relative).
 
-Transport is torch.distributed: NCCL over NVLink/NVSwitch on B200 ranks (the
-moment table is 3 MB at cfg2, tens of microseconds), gloo on CPU for the
-host-logic tests. The plan object only needs the stage interface
-(set_shard / shard_range / stage_device / moments_view), so the same
-orchestration runs against the CUDA plan (FktPlan) and, in the CPU tests, a
-dense stand-in with the same interface.
+Two transports:
+
+* NCCL process groups with the CUDA plan: the whole MVM is ONE library call
+  (fkt_plan_multiply_sharded, csrc/multigpu.cu) on the library's own NCCL
+  communicator (its id shared once over the process group): gather, S2M,
+  moment all-reduce, near + M2T, a broadcast of every rank's owned z range
+  (tree order; no all-reduce of mostly-zero z) and the scatter, captured as
+  one CUDA graph, so a step is one graph launch.
+* any other group (gloo; CPU tensors or CUDA tensors staged through the
+  host): the stage-by-stage orchestration below with torch.distributed
+  collectives. The plan object only needs the stage interface (set_shard /
+  shard_range / stage_device / moments_view), so it runs against the CUDA
+  plan and, in the CPU tests, a dense stand-in with the same interface.
 """
 from __future__ import annotations
 
@@ -39,7 +46,7 @@ class ShardedPlan:
     other rank. group: a torch.distributed process group (default: WORLD).
     """
 
-    def __init__(self, plan, group=None):
+    def __init__(self, plan, group=None, native: Optional[bool] = None):
         import torch.distributed as dist
 
         self.plan = plan
@@ -48,6 +55,41 @@ class ShardedPlan:
         self.world = dist.get_world_size(group)
         plan.set_shard(self.rank, self.world)
         self._buf = None
+        self._comm = None
+        # the one-call NCCL path: a CUDA plan on an NCCL process group
+        if native is None:
+            native = dist.get_backend(group) == "nccl" and hasattr(plan, "_h")
+        if native:
+            self._comm = self._nccl_comm()
+
+    def _nccl_comm(self):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _check, lib
+
+        idb = C.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib.fkt_nccl_unique_id(idb))
+        box = [idb.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=self.group)
+        comm = C.c_void_p()
+        _check(lib.fkt_nccl_comm_create(box[0], self.world, self.rank, C.byref(comm)))
+        return comm
+
+    def close(self):
+        if self._comm is not None:
+            from . import lib
+
+            lib.fkt_nccl_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def shard_range(self):
         return self.plan.shard_range()
@@ -62,6 +104,15 @@ class ShardedPlan:
         nrhs = 1 if y.dim() == 1 else int(y.shape[0])
         if z is None:
             z = torch.empty_like(y)
+        if self._comm is not None and gather:
+            import ctypes as C
+
+            from . import _check, lib
+
+            st = stream if stream is not None else torch.cuda.current_stream()
+            _check(lib.fkt_plan_multiply_sharded(self.plan._h, C.c_void_p(y.data_ptr()), C.c_void_p(z.data_ptr()), nrhs,
+                                                 self._comm, C.c_void_p(st.cuda_stream)))
+            return z
         cuda = y.is_cuda
         st = (stream if stream is not None else torch.cuda.current_stream()) if cuda else None
         ctx = torch.cuda.stream(st) if cuda else contextlib.nullcontext()
@@ -90,7 +141,7 @@ class ShardedPlan:
 
 
 def shard_cuts(leaf_end, leaf_cum_cost, shards: int, n: int):
-    """The library's cut rule (fkt_shard_cuts): leaf-aligned cuts balancing the
+    """The library's host cut rule (fkt_shard_cuts): cuts at the given boundaries balancing the
     cumulative per-leaf cost. Host only."""
     import ctypes as C
 
