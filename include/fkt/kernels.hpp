@@ -13,6 +13,9 @@
 #include <string>
 #include <vector>
 
+#include "fkt/jet.hpp"
+#include "fkt/laurent.hpp"
+
 namespace fkt {
 
 class SingularAtZeroError : public std::domain_error {
@@ -43,6 +46,11 @@ class IsotropicKernel {
   // value-at-zero arguments (kernels.hpp:32-42).
   IsotropicKernel(std::string name, Params params, std::function<double(double)> eval,
                   std::optional<double> valueAtZero);
+  // The reference's full constructor (kernels.hpp:32-42): evaluator, jet
+  // evaluator, registered recurrence, value at zero (host-only, as above).
+  IsotropicKernel(std::string name, Params params, std::function<double(double)> eval,
+                  std::function<Jet(const Jet&)> evalJet, std::optional<RationalLaurent> recurrence,
+                  std::optional<double> valueAtZero);
 
   const std::string& name() const { return name_; }
   const Params& parameters() const { return params_; }
@@ -53,6 +61,12 @@ class IsotropicKernel {
   double evalPositive(double r) const;
   bool hasDerivativeRecurrence() const { return recurrence_; }
   std::optional<double> valueAtZero() const { return valueAtZero_; }
+  // Jet of K at r > 0: coefficient m is K^(m)(r) / m! (kernels.hpp:61-64).
+  Jet jetAt(double r, int order) const;
+  // K on a jet argument (kernels.hpp:66).
+  Jet evalJet(const Jet& r) const;
+  // The registered recurrence K' = q K with exact rational q (kernels.hpp:68).
+  const std::optional<RationalLaurent>& derivativeRecurrence() const { return recurrenceQ_; }
 
  private:
   std::string name_;
@@ -61,6 +75,8 @@ class IsotropicKernel {
   bool recurrence_ = false;
   std::optional<double> valueAtZero_;
   std::function<double(double)> eval_;
+  std::function<Jet(const Jet&)> evalJet_;
+  std::optional<RationalLaurent> recurrenceQ_;
 };
 
 using KernelPtr = std::shared_ptr<const IsotropicKernel>;
@@ -69,6 +85,9 @@ using KernelPtr = std::shared_ptr<const IsotropicKernel>;
 // parameters throw std::invalid_argument.
 KernelPtr makeKernel(const std::string& name, const IsotropicKernel::Params& params = {});
 std::vector<std::string> builtinKernelNames();
+
+// Registered derivative recurrence, if any (kernels.hpp:89).
+std::optional<RationalLaurent> detectDerivativeRecurrence(const IsotropicKernel& kernel);
 
 }  // namespace fkt
 

@@ -85,6 +85,18 @@ int fkt_kernel_check(const char* name, const char* const* keys, const double* va
 int fkt_kernel_eval(const char* name, const char* const* keys, const double* values, int nparams,
                     const double* r, double* out, long long count, int has_diagonal, double diagonal);
 
+/* The registered derivative recurrence K' = q K of a built-in kernel
+ * (kernels.hpp:68, kernels.cpp:37-156) as exact rational Laurent terms: writes
+ * up to max_terms (power, "num/den") pairs, text NUL-separated into buf of
+ * buf_len bytes; *terms = the count (0 and FKT_OK when the kernel has none). */
+int fkt_kernel_recurrence(const char* name, const char* const* keys, const double* values, int nparams, int* terms,
+                          int* powers, int max_terms, char* buf, long long buf_len);
+
+/* K on a jet argument (kernels.hpp:61-66): in = coefficients c_0..c_order of
+ * the argument series at `center`, out = those of K(argument). */
+int fkt_kernel_eval_jet(const char* name, const char* const* keys, const double* values, int nparams, double center,
+                        int order, const double* in, double* out);
+
 void fkt_default_options(fkt_options* opt);
 
 /* fkt::FktPlan(PointCloud, KernelPtr, FktOptions) — transform.cpp:39-92.

@@ -92,6 +92,8 @@ SIGNATURES = {
     "fkt_kernel_check": (C.c_int, C.c_char_p, _cstrs, _d, C.c_int, _i32, _i32, _d),
     "fkt_kernel_eval": (C.c_int, C.c_char_p, _cstrs, _d, C.c_int, _d, _d, C.c_longlong, C.c_int, C.c_double),
     "fkt_default_options": (None, C.POINTER(FktOptionsC)),
+    "fkt_kernel_eval_jet": (C.c_int, C.c_char_p, _cstrs, _d, C.c_int, C.c_double, C.c_int, _d, _d),
+    "fkt_kernel_recurrence": (C.c_int, C.c_char_p, _cstrs, _d, C.c_int, _i32, _i32, C.c_int, C.c_char_p, C.c_longlong),
     "fkt_plan_create": (C.c_int, C.c_int, C.c_int, _d, C.c_char_p, _cstrs, _d, C.c_int,
                         C.POINTER(FktOptionsC), C.POINTER(C.c_void_p)),
     "fkt_plan_destroy": (C.c_int, C.c_void_p),

@@ -71,12 +71,58 @@ IsotropicKernel::IsotropicKernel(std::string name, Params params) : name_(std::m
   check(fkt_kernel_check(name_.c_str(), pa.k(), pa.v(), pa.n(), &rec, &hv0, &v0));
   recurrence_ = rec != 0;
   if (hv0) valueAtZero_ = v0;
+  if (recurrence_) {
+    int terms = 0;
+    int powers[16];
+    std::vector<char> buf(1 << 16);
+    check(fkt_kernel_recurrence(name_.c_str(), pa.k(), pa.v(), pa.n(), &terms, powers, 16, buf.data(),
+                                static_cast<long long>(buf.size())));
+    RationalLaurent q;
+    const char* s = buf.data();
+    for (int i = 0; i < terms; ++i) {
+      const std::string t(s);
+      s += t.size() + 1;
+      const size_t slash = t.find('/');
+      q.add(powers[i], ExactRational{t.substr(0, slash), t.substr(slash + 1)});
+    }
+    recurrenceQ_ = std::move(q);
+  }
 }
 
 IsotropicKernel::IsotropicKernel(std::string name, Params params, std::function<double(double)> eval,
                                  std::optional<double> valueAtZero)
     : name_(std::move(name)), params_(std::move(params)), builtin_(false), valueAtZero_(valueAtZero),
       eval_(std::move(eval)) {}
+
+IsotropicKernel::IsotropicKernel(std::string name, Params params, std::function<double(double)> eval,
+                                 std::function<Jet(const Jet&)> evalJet, std::optional<RationalLaurent> recurrence,
+                                 std::optional<double> valueAtZero)
+    : name_(std::move(name)), params_(std::move(params)), builtin_(false), recurrence_(recurrence.has_value()),
+      valueAtZero_(valueAtZero), eval_(std::move(eval)), evalJet_(std::move(evalJet)),
+      recurrenceQ_(std::move(recurrence)) {}
+
+Jet IsotropicKernel::evalJet(const Jet& r) const {
+  if (!builtin_) {
+    if (!evalJet_) throw std::invalid_argument("kernel '" + name_ + "' has no jet evaluator");
+    return evalJet_(r);
+  }
+  ParamArrays pa(params_);
+  Jet out(r.center(), r.order());
+  std::vector<double> o(static_cast<std::size_t>(r.order()) + 1);
+  check(fkt_kernel_eval_jet(name_.c_str(), pa.k(), pa.v(), pa.n(), r.center(), r.order(), r.coefficients().data(),
+                            o.data()));
+  for (int i = 0; i <= r.order(); ++i) out.coeff(i) = o[static_cast<std::size_t>(i)];
+  return out;
+}
+
+Jet IsotropicKernel::jetAt(double r, int order) const {
+  if (r <= 0.0) throw std::invalid_argument("kernel jet requires r > 0");
+  return evalJet(Jet::variable(r, order));
+}
+
+std::optional<RationalLaurent> detectDerivativeRecurrence(const IsotropicKernel& kernel) {
+  return kernel.derivativeRecurrence();
+}
 
 double IsotropicKernel::evalPositive(double r) const {
   if (!builtin_) return eval_(r);

@@ -153,6 +153,37 @@ int fkt_kernel_eval(const char* name, const char* const* keys, const double* val
   });
 }
 
+int fkt_kernel_recurrence(const char* name, const char* const* keys, const double* values, int nparams, int* terms,
+                          int* powers, int max_terms, char* buf, long long buf_len) {
+  return guarded([&] {
+    const fktb::KernelSpec k = fktb::makeKernelSpec(name, toParams(keys, values, nparams));
+    *terms = 0;
+    if (!k.recurrence) return;
+    std::string text;
+    int i = 0;
+    for (const auto& [p, c] : k.recurrence->terms()) {
+      if (i >= max_terms) throw std::invalid_argument("recurrence: more terms than max_terms");
+      powers[i++] = p;
+      text += c.num().str() + "/" + c.den().str();
+      text.push_back('\0');
+    }
+    if (static_cast<long long>(text.size()) > buf_len) throw std::invalid_argument("recurrence: buffer too small");
+    std::memcpy(buf, text.data(), text.size());
+    *terms = i;
+  });
+}
+
+int fkt_kernel_eval_jet(const char* name, const char* const* keys, const double* values, int nparams, double center,
+                        int order, const double* in, double* out) {
+  return guarded([&] {
+    const fktb::KernelSpec k = fktb::makeKernelSpec(name, toParams(keys, values, nparams));
+    fkt::Jet arg(center, order);
+    for (int i = 0; i <= order; ++i) arg.coeff(i) = in[i];
+    const fkt::Jet r = fktb::kernelJetHost(k, arg);
+    for (int i = 0; i <= order; ++i) out[i] = r.coeff(i);
+  });
+}
+
 void fkt_default_options(fkt_options* o) {
   o->p = 4;
   o->theta = 0.75;

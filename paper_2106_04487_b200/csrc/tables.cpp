@@ -231,6 +231,28 @@ double kernelEvalHost(const KernelSpec& k, double r) {
   throw std::invalid_argument("kernelEvalHost: unknown kernel id");
 }
 
+// K on a jet argument (host; the formulas of kernelEvalHost in jet
+// arithmetic, reference kernels.hpp:61-66).
+fkt::Jet kernelJetHost(const KernelSpec& k, const fkt::Jet& r) {
+  switch (k.id) {
+    case FKTB_KERNEL_EXPONENTIAL: return exp(-r);
+    case FKTB_KERNEL_MATERN12: return k.s2 * exp(-(r / k.rho));
+    case FKTB_KERNEL_MATERN32: return k.s2 * ((1.0 + k.a * r) * exp(-(k.a * r)));
+    case FKTB_KERNEL_CAUCHY: return reciprocal(1.0 + (r * r) * k.is2);
+    case FKTB_KERNEL_RATIONAL_QUADRATIC: return pow(1.0 + (r * r) * k.is2, -0.5);
+    case FKTB_KERNEL_GAUSSIAN: return exp(-(r * r));
+    case FKTB_KERNEL_INVERSE_R: return reciprocal(r);
+    case FKTB_KERNEL_INVERSE_R2: return reciprocal(r * r);
+    case FKTB_KERNEL_INVERSE_R3: return reciprocal(r * r * r);
+    case FKTB_KERNEL_EXP_OVER_R: return exp(-r) / r;
+    case FKTB_KERNEL_R_EXP: return r * exp(-r);
+    case FKTB_KERNEL_COS_OVER_R: return cos(r) / r;
+    case FKTB_KERNEL_EXP_NEG_INV_R: return exp(-reciprocal(r));
+    case FKTB_KERNEL_EXP_NEG_INV_R2: return exp(-reciprocal(r * r));
+  }
+  throw std::invalid_argument("kernelJetHost: unknown kernel id");
+}
+
 void fillKernelDesc(const KernelSpec& k, FktbKernelDesc& out) {
   out.id = k.id;
   out.pad_ = 0;

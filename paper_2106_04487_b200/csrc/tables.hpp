@@ -10,6 +10,7 @@
 #ifndef FKTB_TABLES_HPP
 #define FKTB_TABLES_HPP
 
+#include "fkt/jet.hpp"
 #include <map>
 #include <optional>
 #include <stdexcept>
@@ -70,6 +71,8 @@ KernelSpec makeKernelSpec(const std::string& name, const std::map<std::string, d
 std::vector<std::string> builtinKernelNames();
 // K(r) for r > 0 (host), same formula as the device evaluator.
 double kernelEvalHost(const KernelSpec& k, double r);
+// K on a jet argument (host).
+fkt::Jet kernelJetHost(const KernelSpec& k, const fkt::Jet& r);
 void fillKernelDesc(const KernelSpec& k, FktbKernelDesc& out);
 
 // ---------------------------------------------------------------------------

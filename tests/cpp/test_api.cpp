@@ -260,7 +260,39 @@ static void gp_pipeline() {  // test_gp.cpp:52-61, 115-123, 141-173 (textbook-CG
   CHECK_THROWS_AS(NoisyOperator(train, k, badNoise), DimensionMismatchError);
 }
 
+static void kernel_jets_and_recurrences() {  // test_kernels.cpp:33-60, :100-110
+  auto e = makeKernel("exponential");
+  const Jet j = e->jetAt(1.0, 3);
+  for (int m = 0; m <= 3; ++m) {
+    const double want = std::exp(-1.0) * (m % 2 ? -1.0 : 1.0) / std::tgamma(m + 1.0);
+    CHECK(std::abs(j.coeff(m) - want) < 1e-15);
+  }
+  CHECK(std::abs(j.derivative(2) - std::exp(-1.0)) < 1e-15);
+  CHECK_THROWS_AS(e->jetAt(0.0, 2), std::invalid_argument);
+  // evalJet on a shifted argument equals jetAt at the shifted centre
+  auto c = makeKernel("cauchy", {{"sigma", 0.8}});
+  const Jet a = c->evalJet(Jet::variable(0.7, 5)), b = c->jetAt(0.7, 5);
+  for (int m = 0; m <= 5; ++m) CHECK(std::abs(a.coeff(m) - b.coeff(m)) <= 1e-15 * (1.0 + std::abs(b.coeff(m))));
+  // recurrences: exact rationals, K' = q K on the jet
+  const auto qe = e->derivativeRecurrence();
+  CHECK(qe && qe->terms().size() == 1 && qe->coeff(0).numerator == "-1" && qe->coeff(0).denominator == "1");
+  auto g = makeKernel("gaussian");
+  CHECK(detectDerivativeRecurrence(*g) && detectDerivativeRecurrence(*g)->coeff(1).numerator == "-2");
+  CHECK(!makeKernel("cauchy")->derivativeRecurrence());
+  CHECK(!makeKernel("matern32")->derivativeRecurrence());
+  auto inv = makeKernel("exp-over-r");
+  const Jet ji = inv->jetAt(1.3, 1);
+  CHECK(std::abs(ji.coeff(1) - (*inv->derivativeRecurrence())(1.3) * ji.coeff(0)) < 1e-14);
+  // the reference's 6-argument constructor (host kernel, not for the GPU)
+  IsotropicKernel custom("custom-exp", {}, [](double r) { return std::exp(-r); },
+                         [](const Jet& r) { return exp(-r); }, qe, 1.0);
+  CHECK(custom.derivativeRecurrence() == qe);
+  CHECK(std::abs(custom.jetAt(1.0, 3).coeff(3) - j.coeff(3)) < 1e-15);
+  CHECK_THROWS_AS(plan(PointCloud(10, 2), std::make_shared<IsotropicKernel>(custom)), UnsupportedOnGpuError);
+}
+
 int main() {
+  kernel_jets_and_recurrences();
   dense_basics();
   single_leaf_exact();
   zero_and_linear();
