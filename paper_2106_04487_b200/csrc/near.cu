@@ -156,7 +156,10 @@ constexpr int nearWStride(int r) { return r == 1 ? 0 : (r + 1) / 2 * 2; }
 // 1) at cfg2 (Matern d=3) 12.54 -> 12.32 ms and cfg4 (inverse-r d=3) 14.10 ->
 // 13.92, but slower for the 5-D Gaussian and 16 RHS, whose rows are wider: on
 // for single-RHS 3-D tiles.
-constexpr bool nearPrefetch(int d, int r) { return d == 3 && r == 1; }
+#ifndef FKTB_NEAR_PREFETCH
+#define FKTB_NEAR_PREFETCH 1
+#endif
+constexpr bool nearPrefetch(int d, int r) { return FKTB_NEAR_PREFETCH && d == 3 && r == 1; }
 
 // ---- plan time: geometry rows --------------------------------------------
 struct RowArgs {
@@ -322,7 +325,19 @@ struct NearSmem {
 
 // Launch bounds: min CTAs per SM for the shapes that want a register cap
 // (round-1 B200 sweeps: the 5-D Gaussian at 16 resident warps per SM).
-constexpr int nearMinBlocks(int kid, int d, int r) { return kid == FKTB_KERNEL_GAUSSIAN && d == 5 && r == 1 ? 16 : 1; }
+// (build-time sweep knob for the Matern-3/2 3-D shape: FKTB_NEAR_MINB_M32)
+#ifndef FKTB_NEAR_MINB_M32
+#define FKTB_NEAR_MINB_M32 1
+#endif
+constexpr int nearMinBlocks(int kid, int d, int r) {
+  return kid == FKTB_KERNEL_GAUSSIAN && d == 5 && r == 1 ? 16
+         : kid == FKTB_KERNEL_MATERN32 && d == 3 && r == 1 ? FKTB_NEAR_MINB_M32
+                                                          : 1;
+}
+#ifndef FKTB_NEAR_UNROLL
+#define FKTB_NEAR_UNROLL 2
+#endif
+constexpr int kNearUnroll = FKTB_NEAR_UNROLL;  // source rows per unrolled step
 
 // One warp per CTA (no CTA-wide barriers: a two-warp version spent 17% of
 // their cycles in the per-chunk barrier at cfg4). Work units are (tile, part):
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
           // row cn is the stage's padding row (loaded, never used)
           double cur[GS], cw[R];
           load(cur, cw, 0);
-#pragma unroll 2
+#pragma unroll kNearUnroll
           for (int s = 0; s < cn; ++s) {
             double nx[GS], nw[R];
             load(nx, nw, s + 1);
@@ -505,7 +520,7 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
             for (int r = 0; r < R; ++r) cw[r] = nw[r];
           }
         } else {
-#pragma unroll 2
+#pragma unroll kNearUnroll
           for (int s = 0; s < cn; ++s) {
             double src[GS], wr[R];
             load(src, wr, s);
