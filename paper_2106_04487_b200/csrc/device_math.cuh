@@ -353,6 +353,12 @@ constexpr int harmonic_offset(int d, int k) {
   return h;
 }
 constexpr int slots_u(int p, int k) { return (p - k) / 2 + 1; }
+// First m with a possibly nonzero T-bar_kjm: in d = 3 the entries with
+// m <= j - k - 2 vanish exactly (10 of 62 at p = 6, 29 of 130 at p = 8;
+// verified entry by entry when a plan is built, plan.cu buildFarParams), so
+// the compiled d = 3 radial weights skip them.
+constexpr int tbarFirstM(int d, int k, int j) { return d == 3 && j - k - 1 > 1 ? j - k - 1 : 1; }
+
 constexpr int slot_base(int p, int k) {
   int s = 0;
   for (int q = 0; q < k; ++q) s += slots_u(p, q);

@@ -184,7 +184,9 @@ __device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict_
   const double kd = __hiloint2double(0x43380000, kb) - kMagicK;     // k, exactly
   const double f = fma(kd, -kStep, -u);                              // e^-u = 2^(k/2^BITS) e^f
   double p;
-  if constexpr (BITS >= 9) {  // |f| <= 1.06 ln2/2^10: degree 3, truncation <= 1.4e-14
+  if constexpr (BITS >= 11) {  // |f| <= 1.06 ln2/2^12: degree 2, truncation <= 8e-13
+    p = 0.5;
+  } else if constexpr (BITS >= 9) {  // |f| <= 1.06 ln2/2^10: degree 3, truncation <= 1.4e-14
     p = fma(f, 1.0 / 6.0, 0.5);
   } else {  // |f| <= 0.53 ln2/2^(BITS-1): degree 4, truncation <= 5e-14 at BITS = 6
     p = fma(f, 1.0 / 24.0, 1.0 / 6.0);

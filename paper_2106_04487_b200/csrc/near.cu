@@ -132,15 +132,6 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(const __grid_constan
 // exp argument far below the exp clamp (no clamp in the pair body).
 constexpr double kGramBound = 128.0;
 
-// Runtime A/B knob: FKTB_NEAR_GRAM=0 forces the difference form everywhere.
-inline bool nearGramEnabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("FKTB_NEAR_GRAM");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 // Source row stride (doubles, even: 16-byte rows for the bulk copies): the
 // geometry of the kernel's forms (D coordinates, + |s|^2 for the unfactored
 // Gram form) and, in the LAST slot, the single-RHS weight (written per
@@ -309,8 +300,11 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
 
 // Sources per pipeline stage: ~10 KB of rows per stage (two stages per
 // one-warp CTA, 8-16 CTAs per SM).
+#ifndef FKTB_NEAR_STAGE_BYTES
+#define FKTB_NEAR_STAGE_BYTES 10240
+#endif
 constexpr int nearChunk(int gs, int rp) {
-  const int c = 10240 / ((gs + rp) * 8);
+  const int c = FKTB_NEAR_STAGE_BYTES / ((gs + rp) * 8);
   return c >= 256 ? 256 : c >= 128 ? 128 : c >= 64 ? 64 : 32;
 }
 
@@ -568,7 +562,7 @@ NearFast nearFastConfig(const DevicePlan& plan) {
   f.sel = !(smooth && kd.diag == f.wf);
   // Gram tiles only without the select (it needs exact r == 0 detection);
   // gramLimit2 < 0 leaves every tile to the difference form.
-  if (FastKernel<KID>::gram && !f.sel && nearGramEnabled())
+  if (FastKernel<KID>::gram && !f.sel)
     f.gramLimit2 = kGramBound / (f.sc * f.sc * (1.0 + t.theta * t.theta));
   return f;
 }

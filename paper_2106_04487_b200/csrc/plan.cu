@@ -72,6 +72,10 @@ void buildFarParams(DevicePlan& plan) {
         fact *= m;
         if (at >= FKTB_TBAR_CAP) throw std::invalid_argument("expansion table exceeds the GPU parameter capacity");
         fp->tb[at++] = table.tbarDouble(k, j, m) * fact;
+        // the compiled d = 3 kernels skip m < tbarFirstM(3, k, j) (far.cu):
+        // those entries must be exact zeros of the table
+        if (d == 3 && m < tbarFirstM(3, k, j) && table.tbarDouble(k, j, m) != 0.0)
+          throw std::logic_error("T-bar zero pattern violated for d = 3");
       }
     }
   if (plan.compressed) {
@@ -460,7 +464,9 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
   if (bh) {
     buildBarnesHut(*plan);
   } else {
-    const char* s2m = std::getenv("FKTB_S2M");  // "direct" keeps the per-node direct S2M (A/B knob)
+    // test hook: "direct" keeps the per-node direct S2M (tests/test_gpu_moments.py
+    // checks the monomial-moment path against it)
+    const char* s2m = std::getenv("FKTB_S2M");
     if (momentsSupported(d, options.p) && !(s2m && std::string(s2m) == "direct")) buildMomentPlan(*plan);
   }
   phase(kPhaseMoments);
