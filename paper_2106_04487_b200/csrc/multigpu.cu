@@ -20,6 +20,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -72,6 +73,11 @@ const NcclApi& nccl() {
   if (!api.error.empty()) throw std::invalid_argument("unsupported on the GPU path (multi-GPU): " + api.error);
   return api;
 }
+
+// Bumped by every communicator destroy: a sharded graph captured before it
+// may reference a freed communicator whose address a new one reuses, so
+// graphs remember the epoch they were captured in and are re-captured.
+std::atomic<unsigned long long> g_commEpoch{0};
 
 void ncclCheck(ncclResult_t r, const char* what) {
   if (r != ncclSuccess)
@@ -129,7 +135,9 @@ void* ncclCommCreate(const char* idBytes, int nranks, int rank) {
 }
 
 void ncclCommRelease(void* comm) {
-  if (comm) nccl().commDestroy(static_cast<ncclComm_t>(comm));
+  if (!comm) return;
+  nccl().commDestroy(static_cast<ncclComm_t>(comm));
+  g_commEpoch.fetch_add(1);
 }
 
 void multiplySharded(DevicePlan& plan, const double* y, double* z, int nrhs, void* commPtr, cudaStream_t st) {
@@ -155,9 +163,10 @@ void multiplySharded(DevicePlan& plan, const double* y, double* z, int nrhs, voi
   // one graph per (y, z, nrhs, stream, communicator): a step is one launch
   const auto key = std::make_tuple(static_cast<const void*>(y), static_cast<const void*>(z), nrhs, st);
   auto it = plan.shardedGraphs.find(key);
-  if (it == plan.shardedGraphs.end() || it->second.second != commPtr) {
+  const unsigned long long epoch = g_commEpoch.load();
+  if (it == plan.shardedGraphs.end() || it->second.comm != commPtr || it->second.epoch != epoch) {
     if (it != plan.shardedGraphs.end()) {
-      cudaGraphExecDestroy(it->second.first);
+      cudaGraphExecDestroy(it->second.exec);
       plan.shardedGraphs.erase(it);
     }
     cudaGraph_t graph = nullptr;
@@ -174,14 +183,14 @@ void multiplySharded(DevicePlan& plan, const double* y, double* z, int nrhs, voi
     const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     FKTB_CUDA(e);
-    it = plan.shardedGraphs.emplace(key, std::make_pair(exec, commPtr)).first;
+    it = plan.shardedGraphs.emplace(key, DevicePlan::ShardedGraph{exec, commPtr, epoch}).first;
   }
-  FKTB_CUDA(cudaGraphLaunch(it->second.first, st));
+  FKTB_CUDA(cudaGraphLaunch(it->second.exec, st));
   markDone(plan, st);
 }
 
 void clearShardedGraphs(DevicePlan& plan) {
-  for (auto& kv : plan.shardedGraphs) cudaGraphExecDestroy(kv.second.first);
+  for (auto& kv : plan.shardedGraphs) cudaGraphExecDestroy(kv.second.exec);
   plan.shardedGraphs.clear();
 }
 

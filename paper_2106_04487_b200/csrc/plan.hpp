@@ -231,8 +231,14 @@ struct DevicePlan {
       graphs;
   unsigned long long graphClock = 0;
   bool useGraphs = true;
-  // sharded multiplies (multigpu.cu): graph per (y, z, nrhs, stream) with its communicator
-  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, std::pair<cudaGraphExec_t, void*>> shardedGraphs;
+  // sharded multiplies (multigpu.cu): graph per (y, z, nrhs, stream) with its
+  // communicator and the communicator epoch it was captured in
+  struct ShardedGraph {
+    cudaGraphExec_t exec;
+    void* comm;
+    unsigned long long epoch;
+  };
+  std::map<std::tuple<const void*, const void*, int, cudaStream_t>, ShardedGraph> shardedGraphs;
   // Deterministic mode (det.cu): per list, the per-target index into the
   // partials (sliced by groups of 32 targets, group offsets); the partials of
   // one pass ([entry][rhs], slotsTotal = near + far entries), z_far, the
