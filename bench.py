@@ -214,16 +214,33 @@ def run_ours(args):
                   fkt.FktOptions(p=c["p"], theta=c["theta"], leafCapacity=c["leaf"], nearPrecision=args.near_precision,
                                  deterministic=args.deterministic))
     plan_s = time.perf_counter() - t0
+    plan_phases = pl.plan_phases()
     # re-plan for moving points (FktPlan.rebuild: same plan, new coordinates
-    # of the same n points, buffers reused): the first rebuild sizes the build
-    # scratch, the second is the steady-state figure reported
+    # of the same n points, buffers reused). The first rebuilds size the build
+    # scratch and the list buffers (with headroom); the steady-state figure is
+    # the median of three further rebuilds, alternating moved / original points
     rng = np.random.default_rng(3)
     x_moved = x + 1e-3 * rng.standard_normal(x.shape) * x.std(axis=0)
-    pl.rebuild(x_moved)
-    t0 = time.perf_counter()
-    pl.rebuild(x)
-    replan_s = time.perf_counter() - t0
-    replan_phases = pl.plan_phases()
+    for i in range(3):
+        pl.rebuild(x_moved if i % 2 == 0 else x)
+    replan_each, replan_phase_each = [], []
+    for i in range(3):
+        t0 = time.perf_counter()
+        pl.rebuild(x if i % 2 == 0 else x_moved)
+        replan_each.append(time.perf_counter() - t0)
+        replan_phase_each.append(pl.plan_phases())
+    mid = replan_each.index(sorted(replan_each)[1])
+    replan_s, replan_phases = replan_each[mid], replan_phase_each[mid]
+    # the same with the moved coordinates already in HBM (fkt_plan_rebuild_device)
+    xd = [torch.from_numpy(x_moved).cuda(), torch.from_numpy(x).cuda()]
+    replan_dev_each = []
+    for i in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pl.rebuild_device(xd[i % 2])
+        replan_dev_each.append(time.perf_counter() - t0)
+    replan_dev_s = sorted(replan_dev_each[1:])[1]
+    del xd
     info = pl.info()
     wcols = w.reshape(n, nrhs) if nrhs > 1 else w
     ydev = torch.from_numpy(np.ascontiguousarray(wcols.T if nrhs > 1 else wcols)).cuda()
@@ -376,8 +393,8 @@ def run_ours(args):
                             else "single GPU"),
             "l2": "inputs larger than L2: far lists %.0f MB + near lists %.0f MB + coordinates %.0f MB per step"
                   % (info["far_total"] * 4 / 1e6, info["near_total"] * 4 / 1e6, n * c["d"] * 8 / 1e6),
-            "plan_seconds": plan_s, "plan_phases": pl.plan_phases(),
-            "replan_seconds": replan_s, "replan_phases": replan_phases,
+            "plan_seconds": plan_s, "plan_phases": plan_phases,
+            "replan_seconds": replan_s, "replan_seconds_each": replan_each, "replan_device_seconds": replan_dev_s, "replan_phases": replan_phases,
             "deterministic": bool(args.deterministic),
             "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
             "near_evals": nev_all, "coefficients": P,

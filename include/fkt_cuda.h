@@ -111,6 +111,11 @@ int fkt_plan_destroy(fkt_plan_t plan);
  * equals fkt_plan_create on x with the plan's kernel and options. Cached plans
  * (fkt_plan_cache_get) are shared and refuse it. */
 int fkt_plan_rebuild(fkt_plan_t plan, const double* x);
+/* The same with the new coordinates already in device memory (row-major
+ * n x d, FP64; e.g. a t-SNE embedding updated on the GPU): no host copy. The
+ * caller's writes to x_dev must have completed (or be ordered before the
+ * plan's work by a device synchronisation); returns once the plan is rebuilt. */
+int fkt_plan_rebuild_device(fkt_plan_t plan, const double* x_dev);
 int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info);
 
 /* Plan cache (the reference rebuilds a plan per call site, e.g.

@@ -356,7 +356,8 @@ class FktPlan:
     def __init__(self, cloud: PointCloud, kernel: IsotropicKernel, options: Optional[FktOptions] = None,
                  _cached: bool = False):
         options = options or FktOptions()
-        self._cloud = PointCloud(cloud.n, cloud.d, cloud.x.copy())
+        self._n, self._d = cloud.n, cloud.d
+        self._cloud_host, self._cloud_dev = PointCloud(cloud.n, cloud.d, cloud.x.copy()), None
         self._kernel = kernel
         if options.barnesHut:  # transform.cpp:44: a Barnes-Hut plan has p = 0
             import dataclasses
@@ -402,14 +403,39 @@ class FktPlan:
         are rebuilt on the GPU reusing the plan's buffers (fkt_plan_rebuild)."""
         x = cloud.x if isinstance(cloud, PointCloud) else np.asarray(cloud, dtype=np.float64)
         x = np.ascontiguousarray(x, dtype=np.float64)
-        if x.ndim != 2 or x.shape != (self._cloud.n, self._cloud.d):
+        if x.ndim != 2 or x.shape != (self._n, self._d):
             raise DimensionMismatchError("rebuild: the cloud must have the plan's n points in d dimensions")
         _check(lib.fkt_plan_rebuild(self._h, _dptr(x)))
-        self._cloud = PointCloud(self._cloud.n, self._cloud.d, x.copy())
+        # cloud() hands out this array (a view of the caller's when it was
+        # already contiguous FP64: no 8nd-byte host copy per re-plan)
+        self._cloud_host, self._cloud_dev = PointCloud(self._n, self._d, x), None
+        self._after_rebuild()
+
+    def rebuild_device(self, x) -> None:
+        """rebuild() with the new coordinates already in device memory: a
+        contiguous float64 CUDA tensor of shape (n, d) (fkt_plan_rebuild_device).
+        Pending work on torch's current stream is waited for first."""
+        import torch
+
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+                and tuple(x.shape) == (self._n, self._d)):
+            raise DimensionMismatchError("rebuild_device: need a contiguous float64 CUDA tensor of shape (n, d)")
+        torch.cuda.current_stream(x.device).synchronize()
+        _check(lib.fkt_plan_rebuild_device(self._h, C.c_void_p(x.data_ptr())))
+        self._cloud_host, self._cloud_dev = None, x  # cloud() copies it back on demand
+        self._after_rebuild()
+
+    def _after_rebuild(self) -> None:
         self._tree = None
         info = _L.FktPlanInfoC()
         _check(lib.fkt_plan_info_get(self._h, C.byref(info)))
         self._info = info
+
+    @property
+    def _cloud(self) -> PointCloud:
+        if self._cloud_host is None:
+            self._cloud_host = PointCloud(self._n, self._d, self._cloud_dev.cpu().numpy())
+        return self._cloud_host
 
     # reference accessors
     def cloud(self) -> PointCloud:

@@ -98,6 +98,7 @@ SIGNATURES = {
                         C.POINTER(FktOptionsC), C.POINTER(C.c_void_p)),
     "fkt_plan_destroy": (C.c_int, C.c_void_p),
     "fkt_plan_rebuild": (C.c_int, C.c_void_p, _d),
+    "fkt_plan_rebuild_device": (C.c_int, C.c_void_p, C.c_void_p),
     "fkt_plan_multiply_sharded": (C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p),
     "fkt_nccl_unique_id": (C.c_int, C.c_char_p),
     "fkt_nccl_comm_create": (C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)),

@@ -259,19 +259,31 @@ int fkt_plan_destroy(fkt_plan_t plan) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+void rebuildGuarded(fkt_plan_t plan, const double* x, bool onDevice) {
+  if (!plan || !x) throw std::invalid_argument("rebuild: null plan or coordinates");
+  if (plan->cached) throw std::invalid_argument("plan is shared by the plan cache: rebuild a plan of your own");
+  auto& p = *plan->plan;
+  std::lock_guard<std::mutex> lock(p.mutex);
+  fktb::rebuildPlan(p, x, onDevice);
+  std::lock_guard<std::mutex> vlock(plan->viewMutex);
+  if (plan->view) {  // the borrowed tree view's materialised sets are stale
+    std::lock_guard<std::mutex> tl(plan->view->mutex);
+    plan->view->farReady = plan->view->nearReady = false;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int fkt_plan_rebuild(fkt_plan_t plan, const double* x) {
-  return guarded([&] {
-    if (!plan || !x) throw std::invalid_argument("rebuild: null plan or coordinates");
-    if (plan->cached) throw std::invalid_argument("plan is shared by the plan cache: rebuild a plan of your own");
-    auto& p = *plan->plan;
-    std::lock_guard<std::mutex> lock(p.mutex);
-    fktb::rebuildPlan(p, x);
-    std::lock_guard<std::mutex> vlock(plan->viewMutex);
-    if (plan->view) {  // the borrowed tree view's materialised sets are stale
-      std::lock_guard<std::mutex> tl(plan->view->mutex);
-      plan->view->farReady = plan->view->nearReady = false;
-    }
-  });
+  return guarded([&] { rebuildGuarded(plan, x, false); });
+}
+
+int fkt_plan_rebuild_device(fkt_plan_t plan, const double* x_dev) {
+  return guarded([&] { rebuildGuarded(plan, x_dev, true); });
 }
 
 }  // extern "C"

@@ -489,7 +489,7 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
 // the shard are rebuilt on the GPU; the kernel tables (T-bar, harmonics,
 // compression) and every buffer are kept, so no cudaMalloc runs once the
 // first rebuild has sized the build scratch. Equals a fresh plan on x.
-void rebuildPlan(DevicePlan& plan, const double* hostX) {
+void rebuildPlan(DevicePlan& plan, const double* x, bool onDevice) {
   const auto t0 = std::chrono::steady_clock::now();
   FKTB_CUDA(cudaStreamSynchronize(plan.stream));
   FKTB_CUDA(cudaStreamSynchronize(plan.side));
@@ -504,8 +504,9 @@ void rebuildPlan(DevicePlan& plan, const double* hostX) {
     tPrev = now;
   };
   DeviceTree& t = *plan.tree;
-  FKTB_CUDA(cudaMemcpyAsync(plan.dX.get(), hostX, plan.dX.bytes(), cudaMemcpyHostToDevice, plan.stream));
-  buildTreeGpu(t, hostX, plan.n, plan.d, plan.options.leafCapacity, plan.stream, plan.dX.get());
+  FKTB_CUDA(cudaMemcpyAsync(plan.dX.get(), x, plan.dX.bytes(), onDevice ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            plan.stream));
+  buildTreeGpu(t, nullptr, plan.n, plan.d, plan.options.leafCapacity, plan.stream, plan.dX.get());
   phase(kPhaseTree);
   computeSetsGpu(t, plan.options.theta);
   phase(kPhaseSets);

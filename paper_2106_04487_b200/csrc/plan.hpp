@@ -257,7 +257,8 @@ std::unique_ptr<DevicePlan> createPlan(int n, int d, const double* hostX, const 
                                        const PlanOptions& options);
 void destroyPlan(DevicePlan* plan);
 // Same plan, new coordinates of the same n points (moving points).
-void rebuildPlan(DevicePlan& plan, const double* hostX);
+// x: row-major n x d, on the host or (onDevice) in device memory
+void rebuildPlan(DevicePlan& plan, const double* x, bool onDevice = false);
 // Multi-GPU (multigpu.cu): NCCL communicators (dlopen'd libnccl) and the
 // sharded MVM with both exchanges in one graph.
 void ncclUniqueIdBytes(char* out128);

@@ -97,3 +97,28 @@ def test_rebuild_errors(fkt):
     cached = fkt.FktPlan(fkt.PointCloud.from_array(x0), fkt.makeKernel("cauchy", {}), fkt.FktOptions(p=4), _cached=True)
     with pytest.raises(fkt.InvalidArgument):
         cached.rebuild(x0)
+
+
+def test_rebuild_device_equals_host_rebuild(fkt):
+    """fkt_plan_rebuild_device: coordinates already in HBM (a t-SNE embedding
+    updated on the GPU); same tree, sets and deterministic z as the host-buffer
+    rebuild, and cloud() returns the new points."""
+    import torch
+
+    x0, y = fkt.synthCloud("mixture", 70000, 2, 5)
+    kw = dict(p=6, theta=0.75, leafCapacity=512, deterministic=True)
+    a = _fresh(fkt, x0, "cauchy", {"sigma": 1.0}, **kw)
+    b = _fresh(fkt, x0, "cauchy", {"sigma": 1.0}, **kw)
+    rng = np.random.default_rng(8)
+    x = x0
+    for it in range(3):
+        x = x + 0.05 * rng.standard_normal(x.shape) * x.std(axis=0)
+        a.rebuild(x)
+        b.rebuild_device(torch.from_numpy(x).cuda())
+        _same_tree(a, b)
+        assert np.array_equal(a.multiply(y), b.multiply(y))
+        np.testing.assert_array_equal(b.cloud().x, x)
+    with pytest.raises(fkt.DimensionMismatchError):
+        b.rebuild_device(torch.zeros(10, 2, dtype=torch.float64, device="cuda"))
+    with pytest.raises(fkt.DimensionMismatchError):
+        b.rebuild_device(torch.from_numpy(x.astype(np.float32)).cuda())
