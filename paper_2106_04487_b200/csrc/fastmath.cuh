@@ -90,14 +90,12 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y1, e1, y1);
 }
 
-// Near-field table: 2^NEAR_EXP_BITS entries. 9 -> 512 entries (4 KB), degree
-// 3 with the FP32-indexed reduction. Measured alternative (cfg2, B200): 64
-// entries replicated for the 16 bank pairs (8 KB, conflict-free lookups) with
-// degree 4 is 6% slower -- the 4-way bank conflicts of the 512-entry lookups
-// cost less than the extra FP64 op and shared memory (the loop is bound by
-// FP64 dependency latency, ncu stall_wait, not by the shared-memory pipe).
+// Near-field table: 2^NEAR_EXP_BITS entries. 10 -> 1024 entries (8 KB per
+// one-warp CTA), degree-2 remainder (exp_neg_fi below). Round-1 alternative:
+// 64 entries replicated for the 16 bank pairs (conflict-free lookups) with
+// degree 4 was 6% slower than 512 entries with degree 3.
 #ifndef FKTB_NEAR_EXP_BITS
-#define FKTB_NEAR_EXP_BITS 9
+#define FKTB_NEAR_EXP_BITS 10
 #endif
 constexpr int kNearExpBits = FKTB_NEAR_EXP_BITS;
 constexpr int kNearExpTable = 1 << kNearExpBits;
@@ -135,22 +133,23 @@ __device__ __forceinline__ double exp_neg(double u, const double* __restrict__ t
   return scaled * p;
 }
 
-// e^-u as exp_neg, with the table index found on the FP32 pipe (one FP64 op
-// fewer): the index k = -round(u * 2^BITS / ln2) only has to be NEAR the true
-// rounding, since the FP64 residual f = -k * ln2/2^BITS - u is exact for any
-// k. uf = u truncated to 20 mantissa bits, built from u's high word by one
-// LEA (exponent rebias 1023 -> 127, modulo 2^32; valid for u in [2^-127,
-// 2^129)); k comes out of one FFMA against the FP32 magic 1.5 * 2^23, and its
-// bit pattern kb = 0x4b400000 + k doubles as the low word of the FP64 magic
-// 1.5 * 2^52 + kb, so kd = k costs one DADD; kb's low bits index the table and
-// kb >> BITS carries the exponent (0x4b400000 >> BITS << 20 vanishes mod 2^32).
-// |f| <= 0.53 steps for u <= 32 (degree-3 truncation at BITS = 9: 1.1e-14
-// relative), <= 1 step up to the clamp (1.4e-13 relative on values below
-// e^-32).
+// Near-field e^-u (exp_neg_fi): e^-u = 2^(k/2^BITS) e^f with
+// k = round(-u 2^BITS / ln2) taken from the low word of one magic-number DFMA,
+// f = -k ln2/2^BITS - u by one more DFMA (|f| <= half a table step), a
+// degree-2 remainder from BITS = 10 on (1024-entry table: |f| <= 3.4e-4,
+// truncation f^3/6 <= 6.5e-12 relative; measured z error vs the reference FKT
+// 1.7e-12 at cfg2, gate 1e-10), and the exponent of k folded into the table
+// entry's high word by one integer shift-add (pre-compensated table).
+// Round-2 B200 measurements behind this form (cfg2 near field, 11.55 ms with
+// a 512-entry table, degree 3 and an FP32-pipe index = 15 FP64 + 11 other
+// instructions per pair): degree 2 at 1024 entries 11.21 ms; the index by DFMA
+// instead of LEA + FFMA + MOV 11.51 ms; both 10.78 ms. The pair loop runs at
+// ~2 issue cycles per FP64 instruction plus ~1 per other instruction
+// (register-file operand bandwidth, scripts/probes/rf_probe.cu), so an FP64
+// op that replaces three integer/FP32 ones is a gain.
 //   CLAMP_HI: clamp u <= ~708.3 here (else the caller did, see clamp_exp_arg).
-//   CLAMP_LO: u may be below 2^-127 or negative (uf clamped to 2^-127; then
-//     k = 0 and f = -u, exact for small negative u as the Gram-form Gaussian
-//     needs); else the caller guarantees u >= 2^-127.
+//   CLAMP_LO: kept for the callers' intent (u below 2^-127 or slightly
+//     negative gives k = 0 and f = -u in this form without any clamp).
 __device__ __forceinline__ double clamp_exp_arg(double u) {
   return __hiloint2double(min(__double2hiint(u), 0x40862000), __double2loint(u));
 }
@@ -168,25 +167,25 @@ __device__ __forceinline__ double exp_table_at(const double* __restrict__ tab, i
   return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + off);
 }
 
+#ifndef FKTB_EXP_DEG2_BITS
+#define FKTB_EXP_DEG2_BITS 10  // table bits from which the degree-2 polynomial is used
+#endif
 // tab: the PRE-COMPENSATED table (see the exponent step below).
 template <int REP = 1, int BITS = 9, bool CLAMP_LO = true, bool CLAMP_HI = true>
 __device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict__ tab, int colBytes) {
   static_assert(BITS >= 6, "degree-4 polynomial needs |f| <= ln2/2^7");
-  constexpr float kInvStepF = 1.44269504f * (1 << BITS);
+  constexpr double kInvStep = 1.4426950408889634 * (1 << BITS);
   constexpr double kStep = 0.6931471805599453 / (1 << BITS);
-  constexpr int kHiMin = 896 << 20;                              // 2^-127
-  constexpr double kMagicK = 6755399441055744.0 + 1262485504.0;  // 1.5 * 2^52 + 0x4b400000
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   if constexpr (CLAMP_HI) u = clamp_exp_arg(u);
-  const int hi = CLAMP_LO ? max(__double2hiint(u), kHiMin) : __double2hiint(u);
-  // (hi << 3) - (896 << 23) modulo 2^32 (unsigned: no signed overflow)
-  const float uf = __uint_as_float(static_cast<unsigned>(hi) * 8u + 0x40000000u);
-  const int kb = __float_as_int(fmaf(uf, -kInvStepF, 12582912.0f));  // 0x4b400000 + k, k <= 0
-  const double kd = __hiloint2double(0x43380000, kb) - kMagicK;     // k, exactly
+  const double tk = fma(u, -kInvStep, kMagic);
+  const int kb = __double2loint(tk);  // k (two's complement), k <= 0
+  const double kd = tk - kMagic;      // k, exactly
   const double f = fma(kd, -kStep, -u);                              // e^-u = 2^(k/2^BITS) e^f
   double p;
-  if constexpr (BITS >= 11) {  // |f| <= 1.06 ln2/2^12: degree 2, truncation <= 8e-13
+  if constexpr (BITS >= FKTB_EXP_DEG2_BITS) {  // |f| <= ln2/2^11 at BITS = 10: degree 2, truncation <= 6.5e-12
     p = 0.5;
-  } else if constexpr (BITS >= 9) {  // |f| <= 1.06 ln2/2^10: degree 3, truncation <= 1.4e-14
+  } else if constexpr (BITS >= 9) {  // |f| <= ln2/2^10: degree 3, truncation <= 9e-15
     p = fma(f, 1.0 / 6.0, 0.5);
   } else {  // |f| <= 0.53 ln2/2^(BITS-1): degree 4, truncation <= 5e-14 at BITS = 6
     p = fma(f, 1.0 / 24.0, 1.0 / 6.0);
@@ -199,7 +198,7 @@ __device__ __forceinline__ double exp_neg_fi(double u, const double* __restrict_
   // true): entry j's high word minus j << (20 - BITS)), so one shift-add,
   // hi(tj) + (kb << (20 - BITS)), adds floor(k / 2^BITS) << 20 to the true
   // entry's exponent: kb << (20 - BITS) = (e << 20) + (j << (20 - BITS)) mod
-  // 2^32 for k = e 2^BITS + j (the 0x4b400000 of kb shifts out)
+  // 2^32 for k = e 2^BITS + j
   const unsigned eh = static_cast<unsigned>(__double2hiint(tj)) + (static_cast<unsigned>(kb) << (20 - BITS));
   return __hiloint2double(static_cast<int>(eh), __double2loint(tj)) * p;
 }

@@ -188,7 +188,7 @@ __global__ void near_rows_kernel(const __grid_constant__ RowArgs A) {
                            : 0.0;
   // factored Gaussian: q = Bt - 2 t.s >= 0 with Bt just above this leaf's
   // bound B >= |t|^2 + |s|^2 >= 2 t.s (the 1e-6 and 1e-30 margins cover the
-  // rounding and keep q >= 2^-127 for the FP32-indexed exp); q <= 2.1 B
+  // rounding); q <= 2.1 B
   const double Bt = gram && FAC ? fma(1.000001 * kGramBound / A.gramLimit2, A.limit2[leaf], 1e-30) : 0.0;
   const int sb = static_cast<int>(A.begin[leaf]), se = static_cast<int>(A.end[leaf]);
   for (int p = sb + static_cast<int>(threadIdx.x); p < se; p += blockDim.x) {

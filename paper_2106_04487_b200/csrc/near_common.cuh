@@ -55,8 +55,7 @@ struct FastKernel {
   template <int REP, bool GRAM = false>
   __device__ static __forceinline__ double eval(double q, const double* tab, int colBytes = 0) {
     // Gram q may round slightly below 0: Matern's sources carry a bias that
-    // covers the rounding (near.cu gramBias; sqrt(q) >= 2^-127 as the
-    // FP32-indexed exp needs), the other Gram kernels take 1 + q. The Gram
+    // covers the rounding (near.cu gramBias), the other Gram kernels take 1 + q. The Gram
     // bound keeps sqrt(q) and 1 + q far below the exp clamp: no clamps here.
     if constexpr (KID == FKTB_KERNEL_MATERN32) {
       double u = GRAM ? sqrt_nr_half(q) : sqrt_nr(q);  // Gram q = 2 r^2

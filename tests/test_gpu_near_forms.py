@@ -79,7 +79,9 @@ def test_gram_single_leaf_equals_dense(fkt, ref, name, prm, d):
     assert g == t == 2
     # the reference's own case (cauchy, sigma 1) holds 1e-13 (test_gpu_reference_suite);
     # longer canonical scales raise the Gram rounding bound B (here B ~ 70)
-    assert fkt.relativeError(pl.multiply(y), ref.dense(x, name, prm, y)) <= 1e-12
+    # the exp kernels' near field uses a 1024-entry table with a degree-2 remainder
+    # (|e^f - p(f)| <= 6.5e-12 relative per pair, fastmath.cuh): 1e-11 here, 1e-10 on z
+    assert fkt.relativeError(pl.multiply(y), ref.dense(x, name, prm, y)) <= 1e-11
 
 
 def test_select_kernels_keep_difference_form(fkt, ref):
