@@ -65,6 +65,7 @@ typedef struct fkt_plan_info {
   int compressed;              /* reference FktPlan::compressed() */
   double plan_seconds;
   long long far_tiles, near_tiles, s2m_tiles;
+  int m2t_cartesian;           /* 1: single-RHS multiplies run the Cartesian (q-form) M2T */
 } fkt_plan_info;
 
 /* Last error message / code of the calling thread. */

@@ -72,6 +72,7 @@ class FktPlanInfoC(C.Structure):
         ("far_tiles", C.c_longlong),
         ("near_tiles", C.c_longlong),
         ("s2m_tiles", C.c_longlong),
+        ("m2t_cartesian", C.c_int),
     ]
 
 

@@ -421,6 +421,7 @@ int fkt_plan_info_get(fkt_plan_t plan, fkt_plan_info* info) {
     info->far_tiles = static_cast<long long>(p.farTilesHost.size());
     info->near_tiles = static_cast<long long>(p.nearTilesHost.size());
     info->s2m_tiles = static_cast<long long>(p.s2mTilesHost.size());
+    info->m2t_cartesian = p.cartP > 0 ? 1 : 0;
   });
 }
 
@@ -464,7 +465,8 @@ int fkt_plan_stage_device(fkt_plan_t plan, int stage, const double* y_dev, doubl
       case 0:
         fktb::launchGatherY(p, y_dev, p.dYp.get(), nrhs, st);
         FKTB_CUDA(cudaMemsetAsync(p.dZp.get(), 0, static_cast<size_t>(p.n) * nrhs * sizeof(double), st));
-        FKTB_CUDA(cudaMemsetAsync(p.dMoments.get(), 0, static_cast<size_t>(p.tree->nodes) * p.P * nrhs * sizeof(double), st));
+        FKTB_CUDA(cudaMemsetAsync(p.dMoments.get(), 0,
+                                  static_cast<size_t>(p.tree->nodes) * fktb::momentStrideMax(p) * nrhs * sizeof(double), st));
         break;
       case 1: fktb::launchS2MAny(p, p.dYp.get(), p.dMoments.get(), nrhs, st); break;
       case 2: fktb::launchNearAny(p, p.dYp.get(), p.dZp.get(), nrhs, st); break;
@@ -529,7 +531,9 @@ int fkt_plan_shard_range(fkt_plan_t plan, long long* pos_lo, long long* pos_hi) 
 int fkt_plan_moments_device(fkt_plan_t plan, double** moments, long long* count_per_rhs) {
   return guarded([&] {
     *moments = plan->plan->dMoments.get();
-    *count_per_rhs = static_cast<long long>(plan->plan->tree->nodes) * plan->plan->P;
+    // the widest row layout (single-RHS passes may hold the Cartesian M2T
+    // coefficients): stage 0 zeroes this whole range
+    *count_per_rhs = static_cast<long long>(plan->plan->tree->nodes) * fktb::momentStrideMax(*plan->plan);
   });
 }
 

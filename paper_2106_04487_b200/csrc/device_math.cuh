@@ -11,6 +11,7 @@
 #ifndef FKTB_DEVICE_MATH_CUH
 #define FKTB_DEVICE_MATH_CUH
 
+#include "cart_layout.hpp"
 #include "fkt_device_types.h"
 
 namespace fktb {

@@ -1,6 +1,10 @@
 // Host tables for the monomial-moment S2M (see moments.hpp).
 #include "moments.hpp"
 
+#include <algorithm>
+
+#include "cart_layout.hpp"
+
 #include <map>
 #include <stdexcept>
 
@@ -206,6 +210,112 @@ MomentTables buildMomentTables(int d, int p, const HarmonicStructure& hs, const 
   }
   out.off[static_cast<std::size_t>(out.count)] = static_cast<int>(out.b.size());
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// Cartesian M2T table (see moments.hpp, cart_layout.hpp).
+namespace {
+
+// Exponent tuples of the monomials with total degree in [lo, hi] over
+// variables 0..nv-1, in the order of the device recursion (far.cu cart_eval):
+// the last variable's power descending, recursively; x_0's power descending.
+void cartEnumerate(int nv, int lo, int hi, std::vector<int>& cur, std::vector<std::vector<int>>& out) {
+  if (nv == 1) {
+    for (int j = hi; j >= lo; --j) {
+      cur[0] = j;
+      out.push_back(cur);
+    }
+    cur[0] = 0;
+    return;
+  }
+  for (int e = hi; e >= 0; --e) {
+    cur[static_cast<std::size_t>(nv) - 1] = e;
+    cartEnumerate(nv - 1, std::max(lo - e, 0), hi - e, cur, out);
+  }
+  cur[static_cast<std::size_t>(nv) - 1] = 0;
+}
+
+double factorialD(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= i;
+  return f;
+}
+
+double multinomialD(const std::vector<int>& a) {
+  int n = 0;
+  for (int v : a) n += v;
+  double r = factorialD(n);
+  for (int v : a) r /= factorialD(v);
+  return r;
+}
+
+}  // namespace
+
+bool cartSupported(int kid, int d, int p) {
+  if (kid != FKTB_KERNEL_MATERN32 && kid != FKTB_KERNEL_GAUSSIAN) return false;
+  switch (d * 100 + p) {  // the compiled shapes (far.cu launchCart)
+    case 304:
+    case 306:
+    case 308:
+    case 504: return true;
+    default: return false;
+  }
+}
+
+std::vector<double> buildCartTable(int d, int p, const FktbKernelDesc& kernel, int& PCart) {
+  PCart = 0;
+  if (!cartSupported(kernel.id, d, p)) return {};
+  const MonomialBasis B(d, p);
+  std::map<std::vector<int>, int> idx;
+  for (int i = 0; i < B.count(); ++i) idx[B.exps[static_cast<std::size_t>(i)]] = i;
+  const int C = B.count();
+  // constant factor of F^(n)(q)/n! (the q-dependent factor is evaluated per pair)
+  auto factor = [&](int n) {
+    if (kernel.id == FKTB_KERNEL_GAUSSIAN) return ((n & 1) ? -1.0 : 1.0) / factorialD(n);  // F = e^-q
+    // Matern-3/2: F^(n) = s2 (a^2/2)^n (-1)^n h_n(u), u = a sqrt(q) (far.cu m2t_cart)
+    double f = kernel.s2 / factorialD(n);
+    for (int i = 0; i < n; ++i) f *= -0.5 * kernel.a * kernel.a;
+    return f;
+  };
+  const bool merged = cart_merged(kernel.id);
+  PCart = cart_total(kernel.id, d, p);
+  std::vector<double> T(static_cast<std::size_t>(PCart) * C, 0.0);
+  std::map<std::vector<int>, int> mergedRow;
+  if (merged) {
+    std::vector<std::vector<int>> order;
+    std::vector<int> cur(static_cast<std::size_t>(d), 0);
+    cartEnumerate(d, 0, p, cur, order);
+    for (std::size_t r = 0; r < order.size(); ++r) mergedRow[order[r]] = static_cast<int>(r);
+  }
+  for (int n = 0; n <= p; ++n) {
+    std::vector<std::vector<int>> order;
+    std::vector<int> cur(static_cast<std::size_t>(d), 0);
+    cartEnumerate(d, cart_block_lo(p, n), n, cur, order);
+    const int base = merged ? 0 : cart_block_offset(kernel.id, d, p, n);
+    for (std::size_t r = 0; r < order.size(); ++r) {
+      const std::vector<int>& beta = order[r];
+      int a = 0;
+      for (int v : beta) a += v;
+      const int i = n - a;  // this term carries |x'|^(2i)
+      // F-factor * binom(n, i) (-2)^a (a!/beta!) * nu_{i,beta},
+      // nu_{i,beta} = sum_{|gamma| = i} (i!/gamma!) mu_{beta + 2 gamma}
+      double c = factor(n) * multinomialD(beta);
+      for (int k = 1; k <= i; ++k) c = c * (n - i + k) / k;
+      for (int k = 0; k < a; ++k) c *= -2.0;
+      const int row = merged ? mergedRow.at(beta) : base + static_cast<int>(r);
+      for (int g = 0; g < C; ++g) {
+        const std::vector<int>& gamma = B.exps[static_cast<std::size_t>(g)];
+        int gs = 0;
+        for (int v : gamma) gs += v;
+        if (gs != i) continue;
+        std::vector<int> al(static_cast<std::size_t>(d));
+        for (int q = 0; q < d; ++q)
+          al[static_cast<std::size_t>(q)] = beta[static_cast<std::size_t>(q)] + 2 * gamma[static_cast<std::size_t>(q)];
+        T[static_cast<std::size_t>(row) * C + static_cast<std::size_t>(idx.at(al))] += c * multinomialD(gamma);
+      }
+    }
+  }
+  return T;
 }
 
 }  // namespace fktb

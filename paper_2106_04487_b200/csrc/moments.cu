@@ -516,8 +516,10 @@ void launchS2MMoments(const DevicePlan& plan, const double* yp, double* moments,
     const size_t smem = static_cast<size_t>(kTcRows) * ((C + 1) & ~1) * sizeof(double);
     if (smem > 48 * 1024)
       FKTB_CUDA(cudaFuncSetAttribute(to_coef_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    to_coef_gemm<<<(R + kTcRows - 1) / kTcRows, 128, smem, st>>>(plan.dMono.get(), plan.dMomTT.get(), moments, R, C,
-                                                               plan.P);
+    // single-RHS passes of plans with a Cartesian M2T: its coefficients
+    const bool cart = cartPass(plan, nrhs);
+    to_coef_gemm<<<(R + kTcRows - 1) / kTcRows, 128, smem, st>>>(
+        plan.dMono.get(), cart ? plan.dCartTT.get() : plan.dMomTT.get(), moments, R, C, momentStride(plan, nrhs));
     FKTB_CUDA(cudaGetLastError());
   }
 }

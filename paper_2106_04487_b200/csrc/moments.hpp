@@ -14,6 +14,7 @@
 
 #include <vector>
 
+#include "fkt_device_types.h"
 #include "tables.hpp"
 
 namespace fktb {
@@ -42,6 +43,14 @@ struct MomentTables {
 // harmonic (Z_k nrm^2); factors for compressed plans (else empty).
 MomentTables buildMomentTables(int d, int p, const HarmonicStructure& hs, const std::vector<RadialFactor>& factors,
                                bool compressed, const std::vector<double>& hscale);
+
+// Cartesian M2T coefficients (far.cu m2t_cart): rows of the map from the
+// monomial moments to the coefficients of the polynomials Q_n(x) (layout and
+// formula in device_math.cuh), in the order the device Horner recursion reads
+// them, with the kernel's constant factor of F^(n)(q)/n! folded in. Returns
+// PCart x count (row-major); empty if the kernel has no Cartesian path.
+std::vector<double> buildCartTable(int d, int p, const FktbKernelDesc& kernel, int& PCart);
+bool cartSupported(int kid, int d, int p);
 
 }  // namespace fktb
 

@@ -92,7 +92,7 @@ void enqueueShardedPass(DevicePlan& plan, const double* y, double* z, int nrhs, 
   FKTB_CUDA(cudaMemsetAsync(plan.dZp.get(), 0, n * nrhs * sizeof(double), st));
   FKTB_CUDA(cudaEventRecord(plan.evGather, st));
   FKTB_CUDA(cudaStreamWaitEvent(plan.side, plan.evGather, 0));
-  const size_t mom = static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs;
+  const size_t mom = static_cast<size_t>(plan.tree->nodes) * momentStride(plan, nrhs) * nrhs;
   FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, mom * sizeof(double), plan.side));
   launchS2MAny(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
   ncclCheck(N.allReduce(plan.dMoments.get(), plan.dMoments.get(), mom, ncclFloat64, ncclSum, comm, plan.side),

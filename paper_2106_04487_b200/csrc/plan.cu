@@ -239,6 +239,27 @@ void buildMomentPlan(DevicePlan& plan) {
     uploadVec(plan.dMomTT, tt, st);
     FKTB_CUDA(cudaStreamSynchronize(st));  // tt is a host temporary
   }
+  {
+    // Cartesian M2T coefficients for the kernels that have the path
+    // (FKTB_M2T_CART=0 keeps the harmonic M2T: A/B and test knob)
+    static const bool cartOn = [] {
+      const char* e = std::getenv("FKTB_M2T_CART");
+      return !(e && e[0] == '0');
+    }();
+    FktbKernelDesc kd;
+    fillKernelDesc(plan.kernel, kd);
+    int pc = 0;
+    std::vector<double> ct;
+    if (cartOn && !plan.options.barnesHut) ct = buildCartTable(d, p, kd, pc);
+    plan.cartP = ct.empty() ? 0 : pc;
+    if (plan.cartP > 0) {
+      std::vector<double> tt(ct.size());
+      for (size_t c = 0; c < static_cast<size_t>(pc); ++c)
+        for (size_t a = 0; a < static_cast<size_t>(mt.count); ++a) tt[a * pc + c] = ct[c * mt.count + a];
+      uploadVec(plan.dCartTT, tt, st);
+      FKTB_CUDA(cudaStreamSynchronize(st));
+    }
+  }
   plan.shiftEntries = static_cast<int>(mt.b.size());
   uploadVec(plan.dShiftOff, mt.off, st);
   uploadVec(plan.dShiftB, mt.b, st);
@@ -364,7 +385,7 @@ void ensureWorkspace(DevicePlan& plan, int nrhs) {
     if (r > 1) plan.dNearW.resize(n * r);
     if (plan.dNearCounter.size() == 0) plan.dNearCounter.resize(2);
   }
-  plan.dMoments.resize(std::max<size_t>(1, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs));
+  plan.dMoments.resize(std::max<size_t>(1, static_cast<size_t>(plan.tree->nodes) * momentStrideMax(plan) * nrhs));
   if (plan.options.deterministic) {
     // + one all-zero row: the padding slots of the per-target sums read it
     plan.dPart.resize(static_cast<size_t>(plan.slotsTotal + 1) * nrhs);
@@ -608,7 +629,8 @@ void enqueuePass(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStr
   FKTB_CUDA(cudaMemsetAsync(plan.dZp.get(), 0, n * nrhs * sizeof(double), st));
   FKTB_CUDA(cudaEventRecord(plan.evGather, st));
   FKTB_CUDA(cudaStreamWaitEvent(plan.side, plan.evGather, 0));
-  FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0, static_cast<size_t>(plan.tree->nodes) * plan.P * nrhs * sizeof(double),
+  FKTB_CUDA(cudaMemsetAsync(plan.dMoments.get(), 0,
+                            static_cast<size_t>(plan.tree->nodes) * momentStride(plan, nrhs) * nrhs * sizeof(double),
                             plan.side));
   launchS2MAny(plan, plan.dYp.get(), plan.dMoments.get(), nrhs, plan.side);
   launchNearAny(plan, plan.dYp.get(), plan.dZp.get(), nrhs, st);

@@ -192,6 +192,11 @@ struct DevicePlan {
   int monoCount = 0;
   std::vector<double> hscaleHost, kappaHost;
   DeviceBuffer<double> dMono, dMomT, dMomTT, dShiftCoef;  // dMomTT: T transposed, count x P
+  // Cartesian (q-form) M2T of single-RHS multiplies (far.cu m2t_cart): the
+  // per-node coefficient count (0: not used by this plan) and the map from the
+  // monomial moments, transposed (count x cartP)
+  int cartP = 0;
+  DeviceBuffer<double> dCartTT;
   int shiftEntries = 0;
   DeviceBuffer<int> dShiftOff, dShiftB, dShiftG, dMonoExps, dLevelNodes, dFarNodes;
   std::vector<FktbTile> p2mTilesHost;
@@ -266,6 +271,12 @@ void* ncclCommCreate(const char* idBytes, int nranks, int rank);
 void ncclCommRelease(void* comm);
 void multiplySharded(DevicePlan& plan, const double* y, double* z, int nrhs, void* comm, cudaStream_t stream);
 void clearShardedGraphs(DevicePlan& plan);
+// Doubles per (rhs, node) row of dMoments in an nrhs-column pass: single-RHS
+// passes of plans with a Cartesian M2T store its coefficients instead of the
+// (k, s, h) moments.
+inline bool cartPass(const DevicePlan& plan, int nrhs) { return plan.cartP > 0 && nrhs == 1; }
+inline int momentStride(const DevicePlan& plan, int nrhs) { return cartPass(plan, nrhs) ? plan.cartP : plan.P; }
+inline int momentStrideMax(const DevicePlan& plan) { return plan.cartP > plan.P ? plan.cartP : plan.P; }
 // z = K y for nrhs column-major right-hand sides; y, z device pointers.
 void multiplyDevice(DevicePlan& plan, const double* y, double* z, int nrhs, cudaStream_t stream);
 // z = K y on host buffers (pinned or pageable), synchronous (hostio.cu).

@@ -87,7 +87,9 @@ def test_bitwise_and_close_to_default(fkt, kind, n, d, name, prm, p, leaf, theta
     Y = rng.standard_normal((n, 3))
     Y[:, 0] = y
     Z = det.multiply(Y)
-    assert np.linalg.norm(Z[:, 0] - z1) <= 1e-13 * np.linalg.norm(z1)
+    # (single-RHS Matern-3/2 / Gaussian plans run the Cartesian M2T, several
+    # columns the harmonic one: the same polynomial evaluated two ways)
+    assert np.linalg.norm(Z[:, 0] - z1) <= 5e-12 * np.linalg.norm(z1)
     assert np.array_equal(det.multiply(Y), Z)
 
 

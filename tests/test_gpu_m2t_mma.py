@@ -2,7 +2,10 @@
 nrhs % 8 == 0 and a basis of <= 64 coefficients take the DMMA GEMM path
 (NT = 2 for nrhs % 16 == 0, else NT = 1 over 8-column groups). Every column is
 checked against the unmodified reference FKT (oracle/_ref) at the 1e-10 gate,
-and against the same plan's single-RHS multiply (the DFMA M2T) at 1e-13."""
+and against the same plan's single-RHS multiply at 5e-12 (Matern-3/2 and
+Gaussian plans run the Cartesian M2T there, a different evaluation of the same
+polynomial: the two agree to 6e-14 for Matern-3/2; the compressed Gaussian's
+harmonic form carries ~1e-12 of its own against the reference)."""
 import numpy as np
 import pytest
 
@@ -30,7 +33,7 @@ def test_mma_m2t_columns(fkt, ref, name, prm, d, p, nrhs, comp):
     for c in range(nrhs):
         col = np.ascontiguousarray(W[:, c])
         assert fkt.relativeError(Z[:, c], rp.multiply(col)) <= 1e-10, (c,)
-        assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 1e-13, (c,)
+        assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 5e-12, (c,)
 
 
 @pytest.mark.parametrize("name,prm,d,p,nrhs,comp", [
@@ -53,4 +56,4 @@ def test_rhs_blocked_p2m_columns(fkt, ref, name, prm, d, p, nrhs, comp):
     for c in (0, nrhs // 2, nrhs - 1):
         col = np.ascontiguousarray(W[:, c])
         assert fkt.relativeError(Z[:, c], rp.multiply(col)) <= 1e-10, (c,)
-        assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 1e-13, (c,)
+        assert fkt.relativeError(Z[:, c], pl.multiply(col)) <= 5e-12, (c,)

@@ -42,8 +42,11 @@ def test_moments_path_equals_direct_path(tmp_path, kind, n, d, name, p, comp):
                        check=True, timeout=600)
         outs[mode] = np.load(f)
     a, b = outs["moments"], outs["direct"]
+    # column 0 is the single-RHS multiply: with the moment path a Gaussian /
+    # Matern-3/2 plan runs the Cartesian M2T there (the direct path keeps the
+    # harmonic one), ~1e-12 apart for the compressed Gaussian
     for c in range(a.shape[1]):
-        assert np.linalg.norm(a[:, c] - b[:, c]) / np.linalg.norm(b[:, c]) <= 1e-12
+        assert np.linalg.norm(a[:, c] - b[:, c]) / np.linalg.norm(b[:, c]) <= (5e-12 if c == 0 else 1e-12)
 
 
 def test_moments_path_matches_reference(fkt, ref):
