@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -434,6 +435,18 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
     }
+    // Coincident (r == 0) pairs only occur inside a leaf: every split sends
+    // equal coordinates to the same child (tree.cpp:93-171), so two points at
+    // the same position share their leaf. Only the parts that hold targets of
+    // the source leaf itself pay for the select (inverse-r at cfg4: 1 of ~25
+    // near leaves per target).
+    bool selPart = false;
+    if constexpr (SEL) {
+      bool mine = false;
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) mine |= tpos[i] >= sb && tpos[i] < se;
+      selPart = __any_sync(0xffffffffu, mine);
+    }
     for (int ci = 0; ci < nch; ++ci) {
       if (lane == 0) {
         if (ci + 1 < nch)
@@ -447,7 +460,10 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
       const double* wv = g + SM::kGeo;
       mbar_wait(bar + st, (phase >> st) & 1u);
       phase ^= 1u << st;
-      if (active) {
+      // the chunk against this lane's TPT targets, with (selTag true) or
+      // without the explicit r == 0 select
+      auto evalChunk = [&](auto selTag) {
+        constexpr bool kSel = decltype(selTag)::value;
         // the pair block of one source row against this lane's TPT targets
         auto pairs = [&](const double(&src)[GS], const double(&wr)[R]) {
 #pragma unroll
@@ -475,7 +491,7 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
             // r == 0 <=> q == kQBias; compared on the high word (integer pipe):
             // any other q is >= ~1e-284 (points closer than ~1e-142 count as
             // coincident, where the FP64 form was already off)
-            if constexpr (SEL) kv = __double2hiint(q) == kQBiasHi ? A.diagCanon : kv;
+            if constexpr (kSel) kv = __double2hiint(q) == kQBiasHi ? A.diagCanon : kv;
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[i][r] = fma(kv, wr[r], acc[i][r]);
           }
@@ -520,6 +536,16 @@ __global__ void __launch_bounds__(32, nearMinBlocks(KID, D, R)) near_stream(cons
             load(src, wr, s);
             pairs(src, wr);
           }
+        }
+      };
+      if (active) {
+        if constexpr (SEL) {
+          if (selPart)
+            evalChunk(std::true_type{});
+          else
+            evalChunk(std::false_type{});
+        } else {
+          evalChunk(std::false_type{});
         }
       }
       if (lane == 0 && ci + 1 == nch) sQ[(k + 2) % 3] = claimed;
