@@ -324,8 +324,14 @@ struct NearSmem {
 #ifndef FKTB_NEAR_MINB_M32
 #define FKTB_NEAR_MINB_M32 1
 #endif
+#ifndef FKTB_NEAR_G5_TPT
+#define FKTB_NEAR_G5_TPT 4   // targets per lane, 5-D Gaussian (sweep knob)
+#endif
+#ifndef FKTB_NEAR_G5_MINB
+#define FKTB_NEAR_G5_MINB 12  // B200 sweep (1024-entry exp table): 8-12 -> 17.03 ms at cfg3, 14-16 -> 18.36
+#endif
 constexpr int nearMinBlocks(int kid, int d, int r) {
-  return kid == FKTB_KERNEL_GAUSSIAN && d == 5 && r == 1 ? 16
+  return kid == FKTB_KERNEL_GAUSSIAN && d == 5 && r == 1 ? FKTB_NEAR_G5_MINB
          : kid == FKTB_KERNEL_MATERN32 && d == 3 && r == 1 ? FKTB_NEAR_MINB_M32
                                                           : 1;
 }
@@ -677,6 +683,8 @@ void launchFastSel(const DevicePlan& plan, const NearFast& f, const double* yp, 
   if (nrhs % 4 == 0) return launchPasses<KID, D, SEL, 2, 4>(plan, f, yp, zp, nrhs, st);
   if (nrhs % 2 == 0) return launchPasses<KID, D, SEL, 4, 2>(plan, f, yp, zp, nrhs, st);
   if constexpr (KID == FKTB_KERNEL_MATERN32 && D == 3 && !SEL) return launchPasses<KID, D, SEL, 8, 1>(plan, f, yp, zp, nrhs, st);
+  if constexpr (KID == FKTB_KERNEL_GAUSSIAN && D == 5 && !SEL && FKTB_NEAR_G5_TPT == 8)
+    return launchPasses<KID, D, SEL, 8, 1>(plan, f, yp, zp, nrhs, st);
   return launchPasses<KID, D, SEL, 4, 1>(plan, f, yp, zp, nrhs, st);
 }
 
