@@ -341,6 +341,15 @@ constexpr int compressed_window_hi(int kid, int p) {
 constexpr int comp_slots(int kid, int p, int k) {
   return kid == FKTB_KERNEL_INVERSE_R ? 1 : (p - k) / 2 + 1;
 }
+// Kernels whose compression rank equals comp_slots at every degree (verified
+// per plan): the fused M2T then needs no per-slot select and its factor rows
+// sit at compile-time offsets.
+constexpr bool comp_rank_exact(int kid) { return kid == FKTB_KERNEL_INVERSE_R; }
+constexpr int comp_slot_base(int kid, int p, int k) {
+  int s = 0;
+  for (int q = 0; q < k; ++q) s += comp_slots(kid, p, q);
+  return s;
+}
 constexpr int comp_degree_lo(int kid, int p, int k) {
   return kid == FKTB_KERNEL_INVERSE_R ? -k : compressed_window_lo(kid, p);
 }

@@ -114,6 +114,7 @@ void buildFarParams(DevicePlan& plan) {
     for (int k = 0; k <= p && fits; ++k) {
       const int kid = plan.kernel.id;
       if (plan.factors[static_cast<size_t>(k)].rank > comp_slots(kid, p, k)) fits = false;
+      if (comp_rank_exact(kid) && plan.factors[static_cast<size_t>(k)].rank != comp_slots(kid, p, k)) fits = false;
       for (const Laurent& F : plan.factors[static_cast<size_t>(k)].target)
         if (F.minPower() < comp_degree_lo(kid, p, k) || F.maxPower() > comp_degree_hi(kid, p, k)) fits = false;
     }
@@ -154,6 +155,24 @@ void buildFarParams(DevicePlan& plan) {
     }
   }
   cudaStream_t st = plan.stream;
+  {
+    // fused M2T at d = 3 (far.cu): its Gegenbauer table holds D_n = n! C_n =
+    // n! kappa_n * (monic value), n = k - m, so the staged moments carry the inverse
+    std::vector<double> ms(static_cast<size_t>(std::max(1, fp->P)), 1.0);
+    if (d == 3)
+      for (int k = 0; k <= p; ++k) {
+        const int nh = fp->hOff[k + 1] - fp->hOff[k], su = (p - k) / 2 + 1;
+        for (int j = 0; j < nh; ++j) {
+          const int h = fp->hOff[k] + j, n = k - cc[static_cast<size_t>(h)];
+          double f = kappaHost[static_cast<size_t>(h)];
+          for (int i = 2; i <= n; ++i) f *= i;
+          for (int s2 = 0; s2 < su; ++s2) ms[static_cast<size_t>(fp->cOff[k] + s2 * nh + j)] = 1.0 / f;
+        }
+      }
+    plan.dM2tScale.resize(ms.size());
+    FKTB_CUDA(cudaMemcpyAsync(plan.dM2tScale.get(), ms.data(), plan.dM2tScale.bytes(), cudaMemcpyHostToDevice, st));
+    FKTB_CUDA(cudaStreamSynchronize(st));  // ms is a host temporary
+  }
   plan.hscaleHost = hscale;
   plan.kappaHost = kappaHost;
   plan.dHScale.resize(hscale.size());

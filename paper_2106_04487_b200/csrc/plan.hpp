@@ -197,6 +197,7 @@ struct DevicePlan {
   // monomial moments, transposed (count x cartP)
   int cartP = 0;
   DeviceBuffer<double> dCartTT;
+  DeviceBuffer<double> dM2tScale;  // P: d = 3 fused M2T moment scale 1 / (n! kappa_n) (far.cu m2t_fused)
   int shiftEntries = 0;
   DeviceBuffer<int> dShiftOff, dShiftB, dShiftG, dMonoExps, dLevelNodes, dFarNodes;
   std::vector<FktbTile> p2mTilesHost;
