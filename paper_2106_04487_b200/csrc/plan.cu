@@ -167,6 +167,12 @@ void buildFarParams(DevicePlan& plan) {
           double f = kappaHost[static_cast<size_t>(h)];
           for (int i = 2; i <= n; ++i) f *= i;
           for (int s2 = 0; s2 < su; ++s2) ms[static_cast<size_t>(fp->cOff[k] + s2 * nh + j)] = 1.0 / f;
+          // compressed Laplace plans: the single target factor F_k = c_k r^-k
+          // (the fused kernel multiplies by r^-(k+1) only)
+          if (plan.compressed && plan.kernel.id == FKTB_KERNEL_INVERSE_R && fp->denseAt >= 0) {
+            const int span = fp->denseHi - fp->denseLo + 1;
+            ms[static_cast<size_t>(fp->cOff[k] + j)] *= fp->fc[fp->denseAt + fp->fOff[k] * span + (-k - fp->denseLo)];
+          }
         }
       }
     plan.dM2tScale.resize(ms.size());
