@@ -398,6 +398,7 @@ def run_ours(args):
             "deterministic": bool(args.deterministic),
             "nodes": info["nodes"], "far_pairs": info["far_total"], "near_pairs": info["near_total"],
             "near_evals": nev_all, "coefficients": P,
+            "m2t": ("cartesian (m2t_cart)" if info.get("m2t_cartesian") and nrhs == 1 else "harmonic"),
         },
         "effective_interactions_per_s": float(n) * n * nrhs / mvm_s,
         "stage_ms": {"gather": stage_ms[0], "s2m": stage_ms[1], "near": stage_ms[2], "m2t": stage_ms[3],

@@ -252,7 +252,7 @@ double multinomialD(const std::vector<int>& a) {
 }  // namespace
 
 bool cartSupported(int kid, int d, int p) {
-  if (kid != FKTB_KERNEL_MATERN32 && kid != FKTB_KERNEL_GAUSSIAN) return false;
+  if (kid != FKTB_KERNEL_MATERN32 && kid != FKTB_KERNEL_GAUSSIAN && kid != FKTB_KERNEL_CAUCHY) return false;
   switch (d * 100 + p) {  // the compiled shapes (far.cu launchCart)
     case 304:
     case 306:
@@ -272,6 +272,11 @@ std::vector<double> buildCartTable(int d, int p, const FktbKernelDesc& kernel, i
   // constant factor of F^(n)(q)/n! (the q-dependent factor is evaluated per pair)
   auto factor = [&](int n) {
     if (kernel.id == FKTB_KERNEL_GAUSSIAN) return ((n & 1) ? -1.0 : 1.0) / factorialD(n);  // F = e^-q
+    if (kernel.id == FKTB_KERNEL_CAUCHY) {  // F = 1 / (1 + is2 q): F^(n)/n! = (-is2)^n F^(n+1)
+      double f = 1.0;
+      for (int i = 0; i < n; ++i) f *= -kernel.is2;
+      return f;
+    }
     // Matern-3/2: F^(n) = s2 (a^2/2)^n (-1)^n h_n(u), u = a sqrt(q) (far.cu m2t_cart)
     double f = kernel.s2 / factorialD(n);
     for (int i = 0; i < n; ++i) f *= -0.5 * kernel.a * kernel.a;

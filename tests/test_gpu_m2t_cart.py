@@ -4,7 +4,8 @@ degree-p Taylor polynomial in the source offset, evaluated per pair as
 sum_n F^(n)(q)/n! Q_n(x). Checked against the unmodified reference FKT
 (expansion.cpp:12-55, 314-355 through oracle/_ref) at the 1e-10 gate, against
 the harmonic M2T of the same plan (a two-column multiply takes it), and for
-bitwise repeatability in deterministic mode."""
+bitwise repeatability in deterministic mode. Kernels: Matern-3/2, Gaussian,
+Cauchy."""
 import numpy as np
 import pytest
 
@@ -19,6 +20,9 @@ CASES = [
     ("gaussian", {}, 3, 6, "on"),
     ("gaussian", {}, 3, 8, "off"),
     ("gaussian", {}, 3, 4, None),
+    ("cauchy", {"sigma": 1.0}, 3, 4, None),                 # cfg1 shape
+    ("cauchy", {"sigma": 0.3}, 3, 6, None),
+    ("cauchy", {"sigma": 2.0}, 5, 4, None),
 ]
 
 
@@ -53,7 +57,7 @@ def test_cartesian_m2t_matches_reference_and_harmonic_path(fkt, ref, name, prm, 
 def test_cartesian_m2t_not_used_for_other_kernels(fkt):
     rng = np.random.default_rng(5)
     x = rng.random((4000, 3))
-    for name, prm, p in [("cauchy", {"sigma": 1.0}, 4), ("inverse-r", {}, 8)]:
+    for name, prm, p in [("rational-quadratic", {"sigma": 1.0}, 4), ("inverse-r", {}, 8)]:
         pl = fkt.plan(fkt.PointCloud.from_array(x), fkt.makeKernel(name, prm), fkt.FktOptions(p=p, leafCapacity=128))
         assert pl.info()["m2t_cartesian"] == 0
     # d = 2 keeps the harmonic form (28 coefficients against 50)
