@@ -252,7 +252,9 @@ double multinomialD(const std::vector<int>& a) {
 }  // namespace
 
 bool cartSupported(int kid, int d, int p) {
-  if (kid != FKTB_KERNEL_MATERN32 && kid != FKTB_KERNEL_GAUSSIAN && kid != FKTB_KERNEL_CAUCHY) return false;
+  if (kid != FKTB_KERNEL_MATERN32 && kid != FKTB_KERNEL_GAUSSIAN && kid != FKTB_KERNEL_CAUCHY &&
+      kid != FKTB_KERNEL_MATERN12 && kid != FKTB_KERNEL_EXPONENTIAL)
+    return false;
   switch (d * 100 + p) {  // the compiled shapes (far.cu launchCart)
     case 304:
     case 306:
@@ -277,9 +279,11 @@ std::vector<double> buildCartTable(int d, int p, const FktbKernelDesc& kernel, i
       for (int i = 0; i < n; ++i) f *= -kernel.is2;
       return f;
     }
-    // Matern-3/2: F^(n) = s2 (a^2/2)^n (-1)^n h_n(u), u = a sqrt(q) (far.cu m2t_cart)
-    double f = kernel.s2 / factorialD(n);
-    for (int i = 0; i < n; ++i) f *= -0.5 * kernel.a * kernel.a;
+    // Matern-3/2 and e^(-a r) (Matern-1/2, exponential): F^(n) = s2 (a^2/2)^n (-1)^n h_n(u),
+    // u = a sqrt(q) (far.cu m2t_cart)
+    const double a = kernel.id == FKTB_KERNEL_MATERN32 ? kernel.a : kernel.id == FKTB_KERNEL_MATERN12 ? 1.0 / kernel.rho : 1.0;
+    double f = (kernel.id == FKTB_KERNEL_EXPONENTIAL ? 1.0 : kernel.s2) / factorialD(n);
+    for (int i = 0; i < n; ++i) f *= -0.5 * a * a;
     return f;
   };
   const bool merged = cart_merged(kernel.id);

@@ -11,8 +11,8 @@ reference's Gegenbauer / harmonic expansion (expansion.cpp:12-55, 263-355)
 evaluates. The near field is summed densely over the reference's own near
 sets, the far field by the formula over its far sets; the total must equal the
 reference FKT to rounding (far tighter than the 1e-10 gate), for the kernels
-with a q-derivative recurrence in the CUDA kernel (Matern-3/2, Gaussian) and
-for Cauchy."""
+with a q-derivative form in the CUDA kernel (Matern-1/2 and -3/2, exponential,
+Gaussian, Cauchy)."""
 import itertools
 import math
 
@@ -42,6 +42,15 @@ def _phi(kernel, prm, q, p):
         F = 1.0 / (1.0 + q * is2)
         for n in range(p + 1):
             out[n] = (-is2) ** n * F ** (n + 1)
+    elif kernel in ("exponential", "matern12"):  # e^(-a r): h_(n+1) = (h_(n-1) + (2n - 1) h_n) / u^2
+        a = 1.0 if kernel == "exponential" else 1.0 / prm["rho"]
+        s2 = 1.0 if kernel == "exponential" else prm["sigma"] ** 2
+        u = a * np.sqrt(q)
+        h = [np.exp(-u), np.exp(-u) / u]
+        for n in range(1, p):
+            h.append((h[n - 1] + (2 * n - 1) * h[n]) / u ** 2)
+        for n in range(p + 1):
+            out[n] = s2 * (a * a / 2) ** n * (-1.0) ** n * h[n] / math.factorial(n)
     else:  # matern32: h_(n+1) = (h_(n-1) + (2n - 3) h_n) / u^2
         a, s2 = math.sqrt(3.0) / prm["rho"], prm["sigma"] ** 2
         u = a * np.sqrt(q)
@@ -58,6 +67,10 @@ def _kernel(kernel, prm, r):
         return np.exp(-r * r)
     if kernel == "cauchy":
         return 1.0 / (1.0 + r * r / prm["sigma"] ** 2)
+    if kernel == "exponential":
+        return np.exp(-r)
+    if kernel == "matern12":
+        return prm["sigma"] ** 2 * np.exp(-r / prm["rho"])
     a = math.sqrt(3.0) / prm["rho"]
     return prm["sigma"] ** 2 * (1 + a * r) * np.exp(-a * r)
 
@@ -67,6 +80,8 @@ def _kernel(kernel, prm, r):
     ("gaussian", {}, 5, 4),
     ("gaussian", {}, 3, 6),
     ("cauchy", {"sigma": 1.0}, 3, 4),
+    ("exponential", {}, 3, 4),
+    ("matern12", {"sigma": 1.2, "rho": 0.4}, 3, 6),
 ])
 def test_q_form_equals_reference_fkt(kernel, prm, d, p):
     from oracle import ref

@@ -4,8 +4,8 @@ degree-p Taylor polynomial in the source offset, evaluated per pair as
 sum_n F^(n)(q)/n! Q_n(x). Checked against the unmodified reference FKT
 (expansion.cpp:12-55, 314-355 through oracle/_ref) at the 1e-10 gate, against
 the harmonic M2T of the same plan (a two-column multiply takes it), and for
-bitwise repeatability in deterministic mode. Kernels: Matern-3/2, Gaussian,
-Cauchy."""
+bitwise repeatability in deterministic mode. Kernels: Matern-1/2 and -3/2,
+exponential, Gaussian, Cauchy."""
 import numpy as np
 import pytest
 
@@ -23,6 +23,10 @@ CASES = [
     ("cauchy", {"sigma": 1.0}, 3, 4, None),                 # cfg1 shape
     ("cauchy", {"sigma": 0.3}, 3, 6, None),
     ("cauchy", {"sigma": 2.0}, 5, 4, None),
+    ("exponential", {}, 3, 6, None),                        # compressed by default (same Taylor polynomial)
+    ("exponential", {}, 3, 4, "off"),
+    ("matern12", {"sigma": 1.2, "rho": 0.3}, 3, 8, None),
+    ("matern12", {"sigma": 0.8, "rho": 0.5}, 5, 4, "off"),
 ]
 
 
