@@ -310,6 +310,38 @@ __global__ void m2m_pairs(const __grid_constant__ MomArgs A, const int* pairs, i
 // memory (even row stride: each thread reads two monomials of a row with one
 // broadcast LDS.128), TT columns read coalesced (L1/L2 resident).
 constexpr int kTcRows = 32;
+// Threads cover (row group, output column): with P < blockDim the 32 staged
+// rows split into G = blockDim / P groups (cfg5: P = 28 -> 4 groups of 8 rows,
+// 112 of 128 threads busy instead of 28). T columns are prefetched four
+// monomials ahead (the loads were the loop's latency).
+template <int RPT>
+__device__ __forceinline__ void to_coef_rows(const double* smu, const double* TT, double* out, int r0, int rows,
+                                             int row0, int c, int C, int CS, int P) {
+  double acc[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
+  int a = 0;
+  for (; a + 3 < C; a += 4) {
+    double t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[j] = TT[static_cast<size_t>(a + j) * P + c];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const double2 m0 = *reinterpret_cast<const double2*>(smu + (row0 + i) * CS + a);
+      const double2 m1 = *reinterpret_cast<const double2*>(smu + (row0 + i) * CS + a + 2);
+      acc[i] = fma(t[3], m1.y, fma(t[2], m1.x, fma(t[1], m0.y, fma(t[0], m0.x, acc[i]))));
+    }
+  }
+  for (; a < C; ++a) {
+    const double t0 = TT[static_cast<size_t>(a) * P + c];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i] = fma(t0, smu[(row0 + i) * CS + a], acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i)
+    if (row0 + i < rows) out[static_cast<size_t>(r0 + row0 + i) * P + c] = acc[i];
+}
+
 __global__ void __launch_bounds__(128) to_coef_gemm(const double* mono, const double* TT, double* out, int R, int C,
                                                    int P) {
   extern __shared__ __align__(16) double smu[];  // [kTcRows][CS], CS = C rounded up to even
@@ -321,27 +353,15 @@ __global__ void __launch_bounds__(128) to_coef_gemm(const double* mono, const do
     smu[i] = rr < rows && a < C ? mono[static_cast<size_t>(r0 + rr) * C + a] : 0.0;
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < P; c += blockDim.x) {
-    double acc[kTcRows];
-#pragma unroll
-    for (int i = 0; i < kTcRows; ++i) acc[i] = 0.0;
-    int a = 0;
-    for (; a + 1 < C; a += 2) {
-      const double t0 = TT[static_cast<size_t>(a) * P + c], t1 = TT[static_cast<size_t>(a + 1) * P + c];
-#pragma unroll
-      for (int i = 0; i < kTcRows; ++i) {
-        const double2 m = *reinterpret_cast<const double2*>(smu + i * CS + a);
-        acc[i] = fma(t1, m.y, fma(t0, m.x, acc[i]));
-      }
-    }
-    if (a < C) {  // odd C
-      const double t0 = TT[static_cast<size_t>(a) * P + c];
-#pragma unroll
-      for (int i = 0; i < kTcRows; ++i) acc[i] = fma(t0, smu[i * CS + a], acc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < kTcRows; ++i)
-      if (i < rows) out[static_cast<size_t>(r0 + i) * P + c] = acc[i];
+  const int T = static_cast<int>(blockDim.x);
+  if (4 * P <= T) {  // four row groups of 8
+    const int g = threadIdx.x / P, c = threadIdx.x - g * P;
+    if (g < 4) to_coef_rows<8>(smu, TT, out, r0, rows, 8 * g, c, C, CS, P);
+  } else if (2 * P <= T) {  // two row groups of 16
+    const int g = threadIdx.x / P, c = threadIdx.x - g * P;
+    if (g < 2) to_coef_rows<16>(smu, TT, out, r0, rows, 16 * g, c, C, CS, P);
+  } else {
+    for (int c = threadIdx.x; c < P; c += T) to_coef_rows<kTcRows>(smu, TT, out, r0, rows, 0, c, C, CS, P);
   }
 }
 
