@@ -1,7 +1,7 @@
 # Round-2 measurement set: default bench line (cfg2, cpu_baseline), the
 # reference arm (full-size reference MVMs), per-config lines, deterministic and
 # FP32 lines, and the ncu launch list of the default command.
-TAG=${1:-r02h}
+TAG=${1:-r02i}
 export TAG
 mkdir -p gpurun_out/$TAG
 python bench.py > gpurun_out/$TAG/bench_default_cfg2.json 2> gpurun_out/$TAG/bench_default_cfg2.err || tail -5 gpurun_out/$TAG/bench_default_cfg2.err
